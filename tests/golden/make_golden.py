@@ -1,0 +1,103 @@
+"""Regenerate the golden fixtures in tests/golden/ from the REFERENCE itself.
+
+Run in the build container (needs /root/reference and `make -C oracle`):
+    python tests/golden/make_golden.py
+Every array stored here was produced by the unmodified reference library
+(oracle/_ref/libddmref.so = /root/reference/proj/core compiled with our FFTW-API shim).
+Inputs are portable: the reference synth generator (mt19937_64 + Box-Muller,
+`synth.cpp:98-132`) and u16 stacks drawn from mt19937_64 >> 48 (oracle.ddm_oracle.random_stack).
+"""
+from __future__ import annotations
+
+import hashlib
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[2]
+sys.path.insert(0, str(ROOT))
+
+from oracle import ddm_oracle as O  # noqa: E402
+from oracle import ref  # noqa: E402
+
+OUT = Path(__file__).resolve().parent
+
+# (width, height, frames, seed, lags) — lags None = all
+STACKS = [
+    (8, 8, 16, 101, None),
+    (16, 16, 64, 103, None),
+    (25, 20, 30, 11, None),
+    (1, 1, 5, 3, None),
+    (3, 5, 7, 4, None),
+    (6, 10, 12, 5, None),
+    (32, 32, 100, 7, None),
+    (50, 50, 100, 9, "log"),   # C5 analogue: non-power-of-two sizes (2 * 5^2)
+    (64, 48, 200, 13, "log"),
+]
+
+SEQ_LENGTHS = [1, 2, 3, 5, 16, 100, 1000, 1024, 4096]
+
+
+def seq_for(n: int, seed: int) -> np.ndarray:
+    u = O.mt19937_64(seed, 2 * n).astype(np.float64) * 2.0 ** -64
+    v = (2.0 * u - 1.0).reshape(n, 2)
+    return v[:, 0] + 1j * v[:, 1]
+
+
+def main() -> None:
+    seqs = {}
+    for n in SEQ_LENGTHS:
+        s = seq_for(n, 40 + n)
+        seqs[f"seq_{n}"] = s
+        for prec in ("f64", "f32"):
+            p = ref.with_ft_sequence(s, prec)
+            seqs[f"d_{prec}_{n}"] = p.d
+            seqs[f"da_{prec}_{n}"] = p.d_a
+            seqs[f"corr_{prec}_{n}"] = p.corr
+    np.savez_compressed(OUT / "sequences.npz", **seqs)
+
+    stacks = {}
+    for (w, h, n, seed, lagmode) in STACKS:
+        key = f"{w}x{h}x{n}_s{seed}"
+        st = O.random_stack(w, h, n, seed)
+        lags = O.log_lags(n) if lagmode == "log" else []
+        stacks[f"lags_{key}"] = np.asarray(lags if lags else range(n), dtype=np.int64)
+        stacks[f"sha_{key}"] = np.frombuffer(hashlib.sha256(st.tobytes()).digest(), np.uint8)
+        for prec in ("f64", "f32"):
+            r = ref.run(st, "with_ft", prec, lags=lags, workers=4)
+            stacks[f"map_{prec}_{key}"] = r.values
+        if lagmode == "log":
+            r = ref.run(st, "without_ft", "f64", lags=lags, workers=4)
+            stacks[f"map_without_f64_{key}"] = r.values
+    np.savez_compressed(OUT / "stacks.npz", **stacks)
+
+    # C1 = configs[0] of BASELINE.json: 64x64 x 128 synthetic frames, reference synth seed 7
+    st = ref.generate(64, 64, 128, particles=100, diffusion=0.5, seed=7)
+    lags = O.log_lags(128)
+    c1 = {"sha": np.frombuffer(hashlib.sha256(st.tobytes()).digest(), np.uint8),
+          "lags": np.asarray(lags, dtype=np.int64),
+          "first_frame": st[0]}
+    for prec in ("f64", "f32"):
+        r = ref.run(st, "with_ft", prec, lags=lags, workers=4)
+        c1[f"map_{prec}"] = r.values
+        c1[f"counters_{prec}"] = np.asarray([r.counters["spatial_ffts"],
+                                             r.counters["temporal_ffts"]], dtype=np.int64)
+    means, counts = ref.azimuthal_average(c1["map_f64"], lags, 64, 64)
+    c1["radial_means_f64"] = means
+    c1["radial_counts"] = counts
+    np.savez_compressed(OUT / "c1_synth_seed7.npz", **c1)
+
+    # synth generator goldens (bit-exact u16), a non-square, non-default parameter set
+    syn = {}
+    for (w, h, n, p, d, seed) in [(48, 40, 6, 30, 0.25, 3), (64, 64, 4, 100, 0.5, 7)]:
+        syn[f"stack_{w}x{h}x{n}_p{p}_s{seed}"] = ref.generate(w, h, n, particles=p,
+                                                              diffusion=d, seed=seed)
+    np.savez_compressed(OUT / "synth.npz", **syn)
+
+    for f in sorted(OUT.glob("*.npz")):
+        print(f.name, f.stat().st_size)
+
+
+if __name__ == "__main__":
+    main()
