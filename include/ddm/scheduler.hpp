@@ -1,0 +1,73 @@
+// ddm-b200: the drop-in entry point `ddm::run` (reference `proj/core/include/ddm/scheduler.hpp`).
+// Algorithm::WithFt runs on the GPU: frames are staged to HBM once, each wave-vector group
+// is one batched spatial pass + one fused temporal launch, results come back lag-major in
+// f64. Group planning, counters, partial files, before_merge and validation keep the
+// reference semantics. WithoutFt / Direct are not part of this accelerated path and raise
+// InputError (scope).
+#ifndef DDM_B200_SCHEDULER_HPP
+#define DDM_B200_SCHEDULER_HPP
+
+#include "ddm/archive.hpp"
+#include "ddm/frame_source.hpp"
+#include "ddm/result_map.hpp"
+
+#include <cstdint>
+#include <filesystem>
+#include <functional>
+#include <optional>
+#include <string>
+#include <utility>
+#include <vector>
+
+namespace ddm {
+
+enum class Algorithm { WithFt, WithoutFt, Direct };
+enum class Precision { F32, F64 };
+
+Algorithm parse_algorithm(const std::string& name);
+Precision parse_precision(const std::string& name);
+std::string to_string(Algorithm algorithm);
+std::string to_string(Precision precision);
+
+std::int64_t bytes_per_complex(Precision precision);
+std::int64_t spectrum_bytes(std::int64_t width, std::int64_t height, Precision precision);
+
+struct MemoryBudget {
+    std::int64_t bytes = 0;
+    Precision precision = Precision::F64;
+    std::int64_t complex_size() const { return bytes_per_complex(precision); }
+};
+
+/// Contiguous wave-vector groups of at most K = floor(bytes / (N * bytes_per_complex)).
+struct GroupPlan {
+    std::int64_t capacity = 0;
+    std::vector<std::pair<std::int64_t, std::int64_t>> groups;
+    std::int64_t group_count() const { return std::int64_t(groups.size()); }
+};
+
+GroupPlan plan_with_ft(std::int64_t q_count, std::int64_t frames, const MemoryBudget& budget);
+
+struct RunConfig {
+    Algorithm algorithm = Algorithm::WithFt;
+    Precision precision = Precision::F64;
+    std::vector<std::int64_t> lags;  // empty = all lags 0..N-1
+    std::optional<double> q_max;
+    std::int64_t memory_bytes = 0;
+    int workers = 2;                 // validated (>= 1); values never depend on it
+    std::filesystem::path out_dir;   // non-empty: partials/ kept here
+    std::function<void(const std::filesystem::path&)> before_merge;
+    int device = 0;                  // CUDA device (b200 extension)
+};
+
+ResultArchive run(FrameSource& source, const RunConfig& config);
+
+/// Run WITH_FT writing the lag-major f64 map straight into `out` (capacity values); the
+/// archive's map.values stays empty. Used by the C-ABI to avoid a second copy.
+ResultArchive run_into(FrameSource& source, const RunConfig& config, double* out,
+                       std::int64_t capacity);
+
+ResultMap merge_partials(const std::vector<std::filesystem::path>& files);
+
+} // namespace ddm
+
+#endif

@@ -1,0 +1,31 @@
+// ddm-b200: Brownian-colloid stack generator, bit-identical to the reference
+// (`proj/core/src/synth.cpp:98-132`: mt19937_64, explicit Box-Muller, periodic wrap,
+// Gaussian blobs truncated at 4 sigma, llround + clamp to u16).
+#ifndef DDM_B200_SYNTH_HPP
+#define DDM_B200_SYNTH_HPP
+
+#include "ddm/image_stack.hpp"
+
+#include <cstdint>
+
+namespace ddm {
+
+struct SynthConfig {
+    std::int64_t particles = 100;
+    double diffusion = 0.5;
+    double psf_sigma = 1.0;
+    double amplitude = 1000.0;
+    double background = 100.0;
+    int width = 64;
+    int height = 64;
+    int frames = 256;
+    double frame_interval = 1.0;
+    std::uint64_t seed = 0;
+    void validate() const;
+};
+
+ImageStack generate(const SynthConfig& config);
+
+} // namespace ddm
+
+#endif

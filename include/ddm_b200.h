@@ -1,0 +1,141 @@
+/*
+ * ddm-b200 C-ABI: the drop-in boundary of the B200 WITH_FT (FFT-in-time) structure-function
+ * path.  Plain pointers and sizes only; no exception or C++ type crosses it.  Every entry
+ * point returns a status:
+ *   0 ok, 1 input (ddm::InputError), 2 plan (ddm::PlanError, device memory), 3 io
+ *   (ddm::IoError), 4 cuda (device failure), 5 internal;
+ * and on failure ddm_b200_last_error() returns a thread-local message.
+ *
+ * The reference (`/root/reference/proj`) is a C++ library with no FFI of its own; each
+ * entry point below names the reference interface it replaces (INTEGRATION.md shows the
+ * ctypes / C++ bindings a maintainer would add).
+ */
+#ifndef DDM_B200_H
+#define DDM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DDM_B200_OK 0
+#define DDM_B200_E_INPUT 1
+#define DDM_B200_E_PLAN 2
+#define DDM_B200_E_IO 3
+#define DDM_B200_E_CUDA 4
+#define DDM_B200_E_INTERNAL 5
+
+/* ddm::RunCounters (proj/core/include/ddm/timing.hpp:38-50) */
+typedef struct ddm_b200_counters {
+    uint64_t spatial_ffts;
+    uint64_t temporal_ffts;
+    uint64_t pairs;
+} ddm_b200_counters;
+
+/* ddm::TimingBreakdown (proj/core/include/ddm/timing.hpp:12-29), seconds */
+typedef struct ddm_b200_timing {
+    double disk, step1, step2, merge, other, total;
+} ddm_b200_timing;
+
+/* Called with the workspace path after partials are written, before the merge
+   (ddm::RunConfig::before_merge, proj/core/include/ddm/scheduler.hpp:90-92). */
+typedef void (*ddm_b200_before_merge_fn)(const char* workspace, void* user);
+
+/* ddm::RunConfig (proj/core/include/ddm/scheduler.hpp:78-93) */
+typedef struct ddm_b200_run_config {
+    int algorithm;          /* 0 = with_ft (the only accelerated algorithm) */
+    int precision;          /* 0 = f32, 1 = f64 */
+    const int64_t* lags;    /* n_lags values, NULL/0 = every lag 0..N-1 */
+    int64_t n_lags;
+    int has_q_max;          /* optional<double> q_max */
+    double q_max;
+    int64_t memory_bytes;   /* group planning budget (plan_with_ft) */
+    int workers;            /* validated >= 1; results never depend on it */
+    const char* out_dir;    /* NULL/"" = temporary workspace */
+    ddm_b200_before_merge_fn before_merge; /* NULL = none */
+    void* before_merge_user;
+    int device;             /* CUDA device ordinal */
+} ddm_b200_run_config;
+
+const char* ddm_b200_last_error(void);
+int ddm_b200_version(int* major, int* minor, int* patch);
+int ddm_b200_device_count(int* count);
+
+/* ddm::pad_length (proj/core/src/temporal.cpp:10-17); -1 if n < 1 */
+int64_t ddm_b200_pad_length(int64_t n);
+/* longest sequence the single-CTA temporal engine accepts for a precision (0 f32, 1 f64) */
+int64_t ddm_b200_max_frames(int precision);
+
+/* ddm::plan_with_ft (proj/core/src/scheduler.cpp:365-384) */
+int ddm_b200_plan_with_ft(int64_t q_count, int64_t frames, int64_t bytes, int precision,
+                          int64_t* capacity, int64_t* groups);
+
+/* ddm::cutoff_set (proj/core/src/spectrum.cpp:65-84): count, and flat indices if non-NULL */
+int ddm_b200_cutoff_set(int width, int height, int has_q_max, double q_max, int64_t* count,
+                        int64_t* flat_out);
+
+/* ddm::run (proj/core/src/scheduler.cpp:413-483) over an in-memory frame-major stack
+   (MemoryFrameSource, frame_source.cpp:15-25).  out_values receives the lag-major f64 map,
+   n_lags x height x (width/2+1) (capacity in doubles); out_lags the resolved lag list. */
+int ddm_b200_run_u16(const uint16_t* pixels, int width, int height, int frames,
+                     double frame_interval, const ddm_b200_run_config* config,
+                     double* out_values, int64_t out_capacity, int64_t* out_lags,
+                     int64_t* out_n_lags, ddm_b200_counters* counters,
+                     ddm_b200_timing* timing);
+/* 8-bit frames (north-star extension; values widened exactly to the u16 path's) */
+int ddm_b200_run_u8(const uint8_t* pixels, int width, int height, int frames,
+                    double frame_interval, const ddm_b200_run_config* config,
+                    double* out_values, int64_t out_capacity, int64_t* out_lags,
+                    int64_t* out_n_lags, ddm_b200_counters* counters,
+                    ddm_b200_timing* timing);
+/* ddm::run over RawStackFileSource (frame_source.cpp:27-78) */
+int ddm_b200_run_raw_stack(const char* path, const ddm_b200_run_config* config,
+                           double* out_values, int64_t out_capacity, int64_t* out_lags,
+                           int64_t* out_n_lags, ddm_b200_counters* counters,
+                           ddm_b200_timing* timing);
+
+/* Device-resident WITH_FT: frames already in HBM (pixel_bytes 2 = u16, 1 = u8), map written
+   to HBM as lag-major [n_lags][height*(width/2+1)] f32 (out_f64 = 0) or f64.  Positions
+   outside a cutoff are left untouched.  Runs on the library's stream for `device`, ordered
+   after `stream` (cudaStream_t, may be NULL) and re-joined to it on return; optional
+   device times of the spatial and temporal kernels. */
+int ddm_b200_run_device(const void* d_frames, int pixel_bytes, int width, int height,
+                        int frames, int precision, const int64_t* lags, int64_t n_lags,
+                        int has_q_max, double q_max, void* d_out, int out_f64, int device,
+                        void* stream, double* spatial_ms, double* temporal_ms,
+                        int* kernel_launches);
+
+/* Batched SequenceEngine<S>::with_ft (proj/core/src/temporal.cpp:77-112): q sequences of n
+   complex values, interleaved (re, im) f64, q-major; the working precision is `precision`
+   (values are rounded to f32 first when precision = 0, as a complex<float> caller would).
+   d / d_a / corr are q x n f64 (d_a and corr may be NULL), restored to the original basis. */
+int ddm_b200_sequences_with_ft(const double* seq, int64_t q, int64_t n, int precision,
+                               int device, double* d, double* d_a, double* corr,
+                               uint64_t* temporal_ffts);
+
+/* ddm::compute_spectra (proj/core/src/spectrum.cpp:29-63) on u16 frames: out is
+   frames x height x (width/2+1) complex, interleaved f64. */
+int ddm_b200_spectra_u16(const uint16_t* pixels, int width, int height, int frames,
+                         int precision, int device, double* out);
+/* ddm::forward_spectrum (proj/core/src/spectrum.cpp:12-27) on one real frame (f64 values). */
+int ddm_b200_forward_spectrum(const double* frame, int width, int height, int precision,
+                              int device, double* out);
+
+/* ddm::azimuthal_average (proj/core/src/analysis.cpp:61-97): map is n_lags x plane f64
+   (host); means n_lags x bins, counts bins; capacity = bins the caller allocated. */
+int ddm_b200_azimuthal(const double* values, int64_t n_lags, int width, int height,
+                       int has_q_max, double q_max, int device, double* means,
+                       int64_t* counts, int64_t capacity, int64_t* bin_count);
+
+/* ddm::generate (proj/core/src/synth.cpp:98-132), bit-identical u16 frames. */
+int ddm_b200_generate(int64_t particles, double diffusion, double psf_sigma, double amplitude,
+                      double background, int width, int height, int frames,
+                      double frame_interval, uint64_t seed, uint16_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

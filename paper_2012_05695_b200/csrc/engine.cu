@@ -1,0 +1,456 @@
+// Device orchestration of the WITH_FT hot path (see engine.hpp).
+//
+// One group (the reference's out-of-core wave-vector slice, `scheduler.cpp:89-171`) is
+//   spatial passes over frame chunks (rows -> L2-resident mid -> columns + corner turn)
+//   -> one temporal launch over all tiles of the group -> lag-major output.
+// Groups exist for drop-in semantics (counters, partial files); with the default budget a
+// run is a single group and never leaves the device between the two steps.
+#include "engine.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "kernels.cuh"
+
+namespace ddm::b200 {
+
+using ddmk::cpx;
+
+void check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+DeviceBuffer::~DeviceBuffer() { release(); }
+
+void DeviceBuffer::release() {
+    if (ptr_) cudaFree(ptr_);
+    ptr_ = nullptr;
+    bytes_ = 0;
+}
+
+void* DeviceBuffer::ensure(size_t bytes) {
+    if (bytes <= bytes_ && ptr_) return ptr_;
+    release();
+    check(cudaMalloc(&ptr_, std::max<size_t>(bytes, 256)), "cudaMalloc");
+    bytes_ = std::max<size_t>(bytes, 256);
+    return ptr_;
+}
+
+namespace {
+
+int64_t pad_len(int64_t n) {
+    int64_t n2 = 1;
+    while (n2 < n) n2 <<= 1;
+    return n2 << 1;
+}
+
+// q-major sequences [q][n] (working precision) -> tile-major spectra layout
+template <typename S>
+__global__ void pack_kernel(const cpx<S>* __restrict__ seq, int64_t q, int n, int T,
+                            cpx<S>* __restrict__ spec) {
+    const int64_t total = q * n;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = i / n;
+        const int m = (int)(i - s * n);
+        const int64_t tile = s / T;
+        spec[(tile * n + m) * T + (s - tile * T)] = seq[i];
+    }
+}
+
+// Diagnostic terms of `SequenceEngine::with_ft` restored to the original basis
+// (`temporal.cpp:96-110`): d_a from the original sequence, corr += Re(conj(mu)(suffix+head))
+// + |mu|^2 (N-m) with prefix sums of the shifted sequence. One warp per sequence; the
+// prefix arrays live in `aux` ([q][n+1] f64 for |s|^2, [q][n+1] complex f64 for t).
+template <typename S>
+__global__ void restore_kernel(const cpx<S>* __restrict__ seq, int64_t q, int n,
+                               const double* __restrict__ mean, double* __restrict__ corr,
+                               double* __restrict__ d_a, double* __restrict__ aux) {
+    const int lane = threadIdx.x & 31;
+    const int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    if (s >= q) return;
+    const cpx<S>* x = seq + s * n;
+    double* cp = aux + s * (int64_t)(n + 1) * 3;  // cp[0..n] power prefix, then (re,im) pairs
+    double* tp = cp + (n + 1);
+    const double mx = mean[2 * s], my = mean[2 * s + 1];
+    const S ox = (S)mx, oy = (S)my;
+    double c_p = 0.0, c_x = 0.0, c_y = 0.0;
+    if (lane == 0) { cp[0] = 0.0; tp[0] = 0.0; tp[1] = 0.0; }
+    for (int n0 = 0; n0 < n; n0 += 32) {
+        const int i = n0 + lane;
+        double p = 0.0, tx = 0.0, ty = 0.0;
+        if (i < n) {
+            const cpx<S> v = x[i];
+            p = (double)v.x * (double)v.x + (double)v.y * (double)v.y;
+            tx = (double)(S)(v.x - ox);
+            ty = (double)(S)(v.y - oy);
+        }
+        for (int o = 1; o < 32; o <<= 1) {
+            const double a = __shfl_up_sync(0xffffffffu, p, o);
+            const double b = __shfl_up_sync(0xffffffffu, tx, o);
+            const double c = __shfl_up_sync(0xffffffffu, ty, o);
+            if (lane >= o) { p += a; tx += b; ty += c; }
+        }
+        if (i < n) {
+            cp[i + 1] = c_p + p;
+            tp[2 * (i + 1)] = c_x + tx;
+            tp[2 * (i + 1) + 1] = c_y + ty;
+        }
+        c_p += __shfl_sync(0xffffffffu, p, 31);
+        c_x += __shfl_sync(0xffffffffu, tx, 31);
+        c_y += __shfl_sync(0xffffffffu, ty, 31);
+    }
+    __syncwarp();
+    const double power = mx * mx + my * my;
+    for (int m = lane; m < n; m += 32) {
+        const double ramp = (double)(n - m);
+        d_a[s * n + m] = (cp[n - m] + (cp[n] - cp[m])) / ramp;
+        const double sx = (tp[2 * n] - tp[2 * m]) + tp[2 * (n - m)];
+        const double sy = (tp[2 * n + 1] - tp[2 * m + 1]) + tp[2 * (n - m) + 1];
+        // Re(conj(mu) * (sx + i sy)) = mx sx + my sy
+        corr[s * n + m] += (mx * sx + my * sy) + power * ramp;
+    }
+}
+
+template <typename S>
+void build_table(std::vector<unsigned char>& out, int len, int count) {
+    out.resize((size_t)count * sizeof(cpx<S>));
+    auto* t = reinterpret_cast<cpx<S>*>(out.data());
+    const double pi = 3.141592653589793238462643383279502884;
+    for (int j = 0; j < count; ++j) {
+        const double a = -2.0 * pi * (double)j / (double)len;
+        t[j] = {(S)std::cos(a), (S)std::sin(a)};
+    }
+}
+
+}  // namespace
+
+Engine::Engine(int device) : device_(device) {
+    check(cudaSetDevice(device_), "cudaSetDevice");
+    check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+    for (auto& e : ev_) check(cudaEventCreate(&e), "cudaEventCreate");
+}
+
+Engine::~Engine() {
+    cudaSetDevice(device_);
+    for (auto& e : ev_)
+        if (e) cudaEventDestroy(e);
+    if (stream_) cudaStreamDestroy(stream_);
+}
+
+Engine& Engine::instance(int device) {
+    static std::mutex m;
+    static std::map<int, std::unique_ptr<Engine>> engines;
+    std::lock_guard<std::mutex> lock(m);
+    auto& e = engines[device];
+    if (!e) e = std::make_unique<Engine>(device);
+    return *e;
+}
+
+const void* Engine::twiddles(int len, bool f64) {
+    auto& slot = tw_[{len, f64 ? 1 : 0}];
+    if (!slot) {
+        std::vector<unsigned char> host;
+        if (f64) build_table<double>(host, len, len);
+        else build_table<float>(host, len, len);
+        slot = std::make_unique<DeviceBuffer>();
+        check(cudaMemcpy(slot->ensure(host.size()), host.data(), host.size(),
+                         cudaMemcpyHostToDevice), "twiddle upload");
+    }
+    return slot->get();
+}
+
+const void* Engine::post_twiddles(int W, bool f64) {
+    auto& slot = post_[{W, f64 ? 1 : 0}];
+    if (!slot) {
+        std::vector<unsigned char> host;
+        if (f64) build_table<double>(host, W, W / 2 + 1);
+        else build_table<float>(host, W, W / 2 + 1);
+        slot = std::make_unique<DeviceBuffer>();
+        check(cudaMemcpy(slot->ensure(host.size()), host.data(), host.size(),
+                         cudaMemcpyHostToDevice), "twiddle upload");
+    }
+    return slot->get();
+}
+
+void* Engine::buffer(const std::string& name, size_t bytes) {
+    auto& b = named_[name];
+    if (!b) b = std::make_unique<DeviceBuffer>();
+    return b->ensure(bytes);
+}
+
+int64_t max_frames(bool f64) {
+    int64_t best = 0;
+    for (int64_t n = 1; n <= (1 << 15); n <<= 1)
+        if (ddmk::temporal_tile((int)n, (int)pad_len(n), f64 ? 8 : 4) > 0) best = n;
+    return best;
+}
+
+uint64_t Engine::run(const RunSpec& sp, PhaseTimes* times) {
+    check(cudaSetDevice(device_), "cudaSetDevice");
+    const int W = sp.W, H = sp.H, N = sp.N;
+    const int Wh = W / 2 + 1;
+    const int64_t plane = (int64_t)H * Wh;
+    const int64_t N2 = pad_len(N);
+    const int sb = sp.f64 ? 8 : 4;
+    const size_t cs = 2 * (size_t)sb;
+    const int T = ddmk::temporal_tile(N, (int)N2, sb);
+    if (T == 0)
+        throw std::length_error("sequence of " + std::to_string(N) +
+                                " frames exceeds the single-CTA temporal engine (max " +
+                                std::to_string(max_frames(sp.f64)) + ")");
+    last_T_ = T;
+
+    // lag slots
+    std::vector<int> lag_index((size_t)N, -1);
+    for (size_t li = 0; li < sp.lags.size(); ++li) lag_index[(size_t)sp.lags[li]] = (int)li;
+    check(cudaMemcpyAsync(lagidx_.ensure((size_t)N * sizeof(int)), lag_index.data(),
+                          (size_t)N * sizeof(int), cudaMemcpyHostToDevice, stream_),
+          "lag upload");
+    // flat -> retained index map (cutoff only)
+    const int* d_slot = nullptr;
+    std::vector<int> slot_of;
+    if (!sp.identity) {
+        slot_of.assign((size_t)plane, -1);
+        for (size_t k = 0; k < sp.flat.size(); ++k) slot_of[(size_t)sp.flat[k]] = (int)k;
+        check(cudaMemcpyAsync(slotmap_.ensure((size_t)plane * sizeof(int)), slot_of.data(),
+                              (size_t)plane * sizeof(int), cudaMemcpyHostToDevice, stream_),
+              "slot upload");
+        d_slot = static_cast<const int*>(slotmap_.get());
+    }
+
+    int64_t gmax = 0;
+    for (auto& g : sp.groups) gmax = std::max(gmax, g.second - g.first);
+    const int64_t tiles_max = (gmax + T - 1) / T;
+    void* d_spec = spec_.ensure((size_t)tiles_max * N * T * cs);
+    // frame chunk whose row-pass output stays in L2 (~48 MB)
+    const size_t per_frame = (size_t)Wh * H * cs;
+    const int F = (int)std::max<int64_t>(1, std::min<int64_t>(N, (48u << 20) / per_frame));
+    last_F_ = F;
+    void* d_mid = mid_.ensure((size_t)F * per_frame);
+
+    ddmk::SpatialArgs sa;
+    sa.frames = sp.d_frames;
+    sa.pixel_bytes = sp.pixel_bytes;
+    sa.W = W;
+    sa.H = H;
+    sa.N = N;
+    sa.mid = d_mid;
+    sa.spec = d_spec;
+    sa.slot_of_flat = d_slot;
+    const int Lr = (W % 2 == 0) ? W / 2 : W;
+    sa.tw_row = {Lr, twiddles(Lr, sp.f64)};
+    sa.tw_post = {W, post_twiddles(W, sp.f64)};
+    sa.tw_col = {H, twiddles(H, sp.f64)};
+
+    ddmk::TemporalArgs ta;
+    ta.spec = d_spec;
+    ta.N = N;
+    ta.N2 = (int)N2;
+    ta.tw = {(int)N2, twiddles((int)N2, sp.f64)};
+    ta.tw_half = {(int)N2 / 2, twiddles((int)N2 / 2, sp.f64)};
+    ta.lag_index = static_cast<const int*>(lagidx_.get());
+    ta.out_f64 = sp.out_f64 ? 1 : 0;
+    const size_t ob = sp.out_f64 ? 8 : 4;
+
+    std::vector<cudaEvent_t> evs;
+    auto mark = [&]() -> cudaEvent_t {
+        cudaEvent_t e = nullptr;
+        if (times) {
+            check(cudaEventCreate(&e), "cudaEventCreate");
+            check(cudaEventRecord(e, stream_), "cudaEventRecord");
+            evs.push_back(e);
+        }
+        return e;
+    };
+
+    uint64_t spatial_passes = 0;
+    for (size_t gi = 0; gi < sp.groups.size(); ++gi) {
+        const int64_t gb = sp.groups[gi].first, gc = sp.groups[gi].second - gb;
+        ddmk::SpecLayout lay;
+        lay.T = T;
+        lay.g_begin = gb;
+        lay.g_count = gc;
+        // slots of a partial tile tail are never written by the spatial pass: zero them so
+        // the temporal kernel transforms zeros there
+        if (gc % T) {
+            const int64_t t0 = gc / T;
+            check(cudaMemsetAsync(static_cast<char*>(d_spec) + (size_t)t0 * N * T * cs, 0,
+                                  (size_t)N * T * cs, stream_), "tail memset");
+        }
+        sa.layout = lay;
+        mark();
+        for (int f0 = 0; f0 < N; f0 += F) {
+            sa.frame0 = f0;
+            sa.nframes = std::min(F, N - f0);
+            check(sp.f64 ? ddmk::launch_spatial<double>(sa, stream_)
+                         : ddmk::launch_spatial<float>(sa, stream_), "spatial kernels");
+            if (times) times->spatial_launches += 2;
+        }
+        mark();
+        spatial_passes += (uint64_t)N;
+
+        ta.layout = lay;
+        if (sp.partial_mode) {
+            ta.out = partial_.ensure((size_t)sp.lags.size() * gc * ob);
+            ta.out_stride = gc;
+            ta.dest_of_slot = nullptr;
+        } else if (sp.identity) {
+            ta.out = static_cast<char*>(sp.d_out) + (size_t)gb * ob;
+            ta.out_stride = sp.out_stride;
+            ta.dest_of_slot = nullptr;
+        } else {
+            check(cudaMemcpyAsync(dest_.ensure((size_t)gc * sizeof(int64_t)), sp.flat.data() + gb,
+                                  (size_t)gc * sizeof(int64_t), cudaMemcpyHostToDevice, stream_),
+                  "dest upload");
+            ta.out = sp.d_out;
+            ta.out_stride = sp.out_stride;
+            ta.dest_of_slot = static_cast<const int64_t*>(dest_.get());
+        }
+        mark();
+        check(sp.f64 ? ddmk::launch_temporal<double>(ta, stream_)
+                     : ddmk::launch_temporal<float>(ta, stream_), "temporal kernel");
+        if (times) times->temporal_launches += 1;
+        mark();
+        if (sp.partial_mode && sp.on_partial) sp.on_partial(gi, ta.out, gc);
+        // the host-side slot map / dest vectors must outlive the async copies
+        if (!sp.identity || sp.partial_mode) check(cudaStreamSynchronize(stream_), "sync");
+    }
+    if (times) {
+        check(cudaStreamSynchronize(stream_), "sync");
+        for (size_t i = 0; i + 3 < evs.size(); i += 4) {
+            float a = 0.f, b = 0.f;
+            cudaEventElapsedTime(&a, evs[i], evs[i + 1]);
+            cudaEventElapsedTime(&b, evs[i + 2], evs[i + 3]);
+            times->spatial_ms += a;
+            times->temporal_ms += b;
+        }
+        for (auto e : evs) cudaEventDestroy(e);
+    } else {
+        // lag_index / slot_of host vectors are consumed by async copies above
+        check(cudaStreamSynchronize(stream_), "sync");
+    }
+    return spatial_passes;
+}
+
+void Engine::spectra(const void* d_frames, int pixel_bytes, int W, int H, int N, bool f64,
+                     void* d_out) {
+    check(cudaSetDevice(device_), "cudaSetDevice");
+    const int Wh = W / 2 + 1;
+    const size_t cs = f64 ? 16 : 8;
+    const size_t per_frame = (size_t)Wh * H * cs;
+    const int F = (int)std::max<int64_t>(1, std::min<int64_t>(N, (48u << 20) / per_frame));
+    ddmk::SpatialArgs sa;
+    sa.frames = d_frames;
+    sa.pixel_bytes = pixel_bytes;
+    sa.W = W;
+    sa.H = H;
+    sa.N = N;
+    sa.mid = mid_.ensure((size_t)F * per_frame);
+    sa.spec = d_out;
+    // one tile holding the whole plane: spec[(0 * N + n) * plane + s] = frame-major output
+    sa.layout.T = (int)((int64_t)H * Wh);
+    sa.layout.g_begin = 0;
+    sa.layout.g_count = (int64_t)H * Wh;
+    const int Lr = (W % 2 == 0) ? W / 2 : W;
+    sa.tw_row = {Lr, twiddles(Lr, f64)};
+    sa.tw_post = {W, post_twiddles(W, f64)};
+    sa.tw_col = {H, twiddles(H, f64)};
+    for (int f0 = 0; f0 < N; f0 += F) {
+        sa.frame0 = f0;
+        sa.nframes = std::min(F, N - f0);
+        check(f64 ? ddmk::launch_spatial<double>(sa, stream_) : ddmk::launch_spatial<float>(sa, stream_),
+              "spatial kernels");
+    }
+    check(cudaStreamSynchronize(stream_), "sync");
+}
+
+void Engine::sequences(const void* d_seq, int64_t q, int64_t n, bool f64, double* d_out,
+                       double* d_a_out, double* corr_out) {
+    check(cudaSetDevice(device_), "cudaSetDevice");
+    const int64_t N2 = pad_len(n);
+    const int sb = f64 ? 8 : 4;
+    const size_t cs = 2 * (size_t)sb;
+    const int T = ddmk::temporal_tile((int)n, (int)N2, sb);
+    if (T == 0)
+        throw std::length_error("sequence of " + std::to_string(n) +
+                                " frames exceeds the single-CTA temporal engine");
+    const int64_t tiles = (q + T - 1) / T;
+    void* d_spec = spec_.ensure((size_t)tiles * n * T * cs);
+    check(cudaMemsetAsync(d_spec, 0, (size_t)tiles * n * T * cs, stream_), "memset");
+    const int threads = 256;
+    const int blocks = (int)std::min<int64_t>(148 * 16, (q * n + threads - 1) / threads);
+    if (f64)
+        pack_kernel<double><<<blocks, threads, 0, stream_>>>(static_cast<const cpx<double>*>(d_seq),
+                                                             q, (int)n, T,
+                                                             static_cast<cpx<double>*>(d_spec));
+    else
+        pack_kernel<float><<<blocks, threads, 0, stream_>>>(static_cast<const cpx<float>*>(d_seq),
+                                                            q, (int)n, T,
+                                                            static_cast<cpx<float>*>(d_spec));
+    check(cudaGetLastError(), "pack kernel");
+
+    std::vector<int> lag_index((size_t)n);
+    for (int64_t m = 0; m < n; ++m) lag_index[(size_t)m] = (int)m;
+    check(cudaMemcpyAsync(lagidx_.ensure((size_t)n * sizeof(int)), lag_index.data(),
+                          (size_t)n * sizeof(int), cudaMemcpyHostToDevice, stream_), "lag upload");
+    // out[s][m]: li = m, dest(s) = s * n, out_stride = 1
+    std::vector<int64_t> dest((size_t)q);
+    for (int64_t s = 0; s < q; ++s) dest[(size_t)s] = s * n;
+    check(cudaMemcpyAsync(dest_.ensure((size_t)q * sizeof(int64_t)), dest.data(),
+                          (size_t)q * sizeof(int64_t), cudaMemcpyHostToDevice, stream_),
+          "dest upload");
+
+    const bool terms = d_a_out || corr_out;
+    double* d_mean = nullptr;
+    double* d_corr = nullptr;
+    double* d_aux = nullptr;
+    if (terms) {
+        const size_t need = (size_t)q * 2 * sizeof(double) + (size_t)q * n * sizeof(double) +
+                            (size_t)q * (n + 1) * 3 * sizeof(double);
+        char* base = static_cast<char*>(seq_aux_.ensure(need));
+        d_mean = reinterpret_cast<double*>(base);
+        d_corr = corr_out ? corr_out : reinterpret_cast<double*>(base + (size_t)q * 2 * sizeof(double));
+        d_aux = reinterpret_cast<double*>(base + (size_t)q * 2 * sizeof(double) +
+                                          (size_t)q * n * sizeof(double));
+    }
+    ddmk::TemporalArgs ta;
+    ta.spec = d_spec;
+    ta.N = (int)n;
+    ta.N2 = (int)N2;
+    ta.layout.T = T;
+    ta.layout.g_begin = 0;
+    ta.layout.g_count = q;
+    ta.tw = {(int)N2, twiddles((int)N2, f64)};
+    ta.tw_half = {(int)N2 / 2, twiddles((int)N2 / 2, f64)};
+    ta.lag_index = static_cast<const int*>(lagidx_.get());
+    ta.out = d_out;
+    ta.out_f64 = 1;
+    ta.out_stride = 1;
+    ta.dest_of_slot = static_cast<const int64_t*>(dest_.get());
+    ta.corr_out = d_corr;
+    ta.mean_out = d_mean;
+    check(f64 ? ddmk::launch_temporal<double>(ta, stream_) : ddmk::launch_temporal<float>(ta, stream_),
+          "temporal kernel");
+    if (terms) {
+        double* d_da = d_a_out ? d_a_out : d_out;  // never both null here when terms
+        std::vector<double> keep;
+        if (!d_a_out) {
+            // d_a not requested: restore into scratch so d_out survives
+            d_da = reinterpret_cast<double*>(user_scratch_.ensure((size_t)q * n * sizeof(double)));
+        }
+        const int rb = (int)((q * 32 + 255) / 256);
+        if (f64)
+            restore_kernel<double><<<rb, 256, 0, stream_>>>(static_cast<const cpx<double>*>(d_seq), q,
+                                                            (int)n, d_mean, d_corr, d_da, d_aux);
+        else
+            restore_kernel<float><<<rb, 256, 0, stream_>>>(static_cast<const cpx<float>*>(d_seq), q,
+                                                           (int)n, d_mean, d_corr, d_da, d_aux);
+        check(cudaGetLastError(), "restore kernel");
+    }
+    check(cudaStreamSynchronize(stream_), "sync");
+}
+
+}  // namespace ddm::b200

@@ -1,0 +1,140 @@
+// Device orchestration of the WITH_FT hot path on one B200 (internal C++ API; the public
+// boundaries are include/ddm_b200.h (C-ABI) and include/ddm/*.hpp (reference-mirroring C++).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <functional>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+namespace ddm::b200 {
+
+// CUDA failure (status 4 at the C-ABI).
+class CudaError : public std::runtime_error {
+public:
+    using std::runtime_error::runtime_error;
+};
+
+void check(cudaError_t e, const char* what);
+
+// Owning device allocation.
+class DeviceBuffer {
+public:
+    DeviceBuffer() = default;
+    ~DeviceBuffer();
+    DeviceBuffer(const DeviceBuffer&) = delete;
+    DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+    void* ensure(size_t bytes);  // grows, never shrinks; contents not preserved
+    void* get() const { return ptr_; }
+    size_t size() const { return bytes_; }
+    void release();
+
+private:
+    void* ptr_ = nullptr;
+    size_t bytes_ = 0;
+};
+
+// Seconds of device time per phase, measured with CUDA events on the engine stream.
+struct PhaseTimes {
+    double spatial_ms = 0.0;
+    double temporal_ms = 0.0;
+    int spatial_launches = 0;
+    int temporal_launches = 0;
+};
+
+struct RunSpec {
+    int W = 0, H = 0, N = 0;
+    bool f64 = false;                 // working precision of the transforms
+    int pixel_bytes = 2;              // 2 = u16, 1 = u8
+    const void* d_frames = nullptr;   // device [N][H][W]
+    std::vector<int64_t> lags;        // sorted, unique, within [0, N)
+    std::vector<int64_t> flat;        // retained flat indices (row*(W/2+1)+col), ascending
+    bool identity = true;             // flat[k] == k for every k (no cutoff)
+    std::vector<std::pair<int64_t, int64_t>> groups;  // [begin, end) over the retained list
+    // Output. Full-map mode: out[li * out_stride + flat[k]] (out_stride = plane), the
+    // caller zero-fills positions outside the cutoff. Partial mode: per group a lag-major
+    // [L][g_count] block (the reference PartialResult layout) handed to on_partial.
+    void* d_out = nullptr;
+    bool out_f64 = true;
+    int64_t out_stride = 0;
+    bool partial_mode = false;
+    std::function<void(size_t group, const void* d_partial, int64_t g_count)> on_partial;
+};
+
+class Engine {
+public:
+    explicit Engine(int device);
+    ~Engine();
+    Engine(const Engine&) = delete;
+    Engine& operator=(const Engine&) = delete;
+
+    int device() const { return device_; }
+    cudaStream_t stream() const { return stream_; }
+
+    // Runs every group of `spec` on the engine stream (asynchronous w.r.t. the host unless
+    // on_partial needs the data). Returns the number of spatial passes (= frames x groups).
+    uint64_t run(const RunSpec& spec, PhaseTimes* times = nullptr);
+
+    // Batched SequenceEngine::with_ft: q sequences of n complex values, q-major on device
+    // (working precision). d_out [q][n] f64; optional d_a / corr [q][n] f64 restored to the
+    // original basis like `temporal.cpp:96-110`.
+    void sequences(const void* d_seq, int64_t q, int64_t n, bool f64, double* d_out,
+                   double* d_a_out, double* corr_out);
+
+    // Batched spatial transform only (`compute_spectra`): frames [N][H][W] (pixel_bytes 2 u16,
+    // 1 u8, 4 f32, 8 f64) -> d_out [N][H][W/2+1] complex in the working precision.
+    void spectra(const void* d_frames, int pixel_bytes, int W, int H, int N, bool f64,
+                 void* d_out);
+
+    // Device staging buffer for frames owned by the engine.
+    void* frame_buffer(size_t bytes) { return frames_.ensure(bytes); }
+    void* scratch(size_t bytes) { return user_scratch_.ensure(bytes); }
+    // Named, growable device buffers owned by the engine (result maps, staging, ...).
+    void* buffer(const std::string& name, size_t bytes);
+
+    // Last spatial-chunk / tile geometry (for reports).
+    int last_tile() const { return last_T_; }
+    int last_chunk_frames() const { return last_F_; }
+
+    std::mutex& mutex() { return mu_; }
+
+    static Engine& instance(int device);
+
+private:
+    const void* twiddles(int len, bool f64);           // exp(-2 pi i j / len), j < len
+    const void* post_twiddles(int W, bool f64);        // exp(-2 pi i k / W), k <= W/2
+
+    int device_;
+    cudaStream_t stream_ = nullptr;
+    cudaEvent_t ev_[4] = {};
+    DeviceBuffer frames_, spec_, mid_, lagidx_, slotmap_, dest_, partial_, user_scratch_;
+    DeviceBuffer seq_aux_;
+    std::map<std::pair<int, int>, std::unique_ptr<DeviceBuffer>> tw_;
+    std::map<std::pair<int, int>, std::unique_ptr<DeviceBuffer>> post_;
+    std::map<std::string, std::unique_ptr<DeviceBuffer>> named_;
+    int last_T_ = 0, last_F_ = 0;
+    std::mutex mu_;
+};
+
+// Hardware limits of the one-CTA temporal kernel (longest supported sequence).
+int64_t max_frames(bool f64);
+
+// Device reduction over n doubles: all finite?, max, min (for ResultArchive::validate).
+void reduce_stats(const double* d, int64_t n, cudaStream_t stream, bool* finite, double* max_v,
+                  double* min_v);
+
+// Deterministic ring average on device (`analysis.cpp:61-97`): values [L][plane] f64 device,
+// bins [plane] int32 (-1 = not retained), order/offsets = retained positions sorted by bin
+// (CSR), means [L][nbins] f64 device.
+void radial_means(const double* d_values, int64_t n_lags, int64_t plane, const int64_t* d_order,
+                  const int64_t* d_offsets, int64_t nbins, double* d_means, cudaStream_t stream);
+
+}  // namespace ddm::b200

@@ -1,0 +1,371 @@
+// extern "C" boundary (include/ddm_b200.h). Every entry point converts the library's
+// exceptions into status codes + a thread-local message; nothing throws across it.
+#include "ddm_b200.h"
+
+#include "ddm/analysis.hpp"
+#include "ddm/errors.hpp"
+#include "ddm/scheduler.hpp"
+#include "ddm/spectrum.hpp"
+#include "ddm/synth.hpp"
+#include "ddm/temporal.hpp"
+#include "run_internal.hpp"
+
+#include <algorithm>
+#include <cstring>
+#include <new>
+#include <string>
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <class Fn>
+int guarded(Fn&& fn) {
+    try {
+        fn();
+        g_last_error.clear();
+        return DDM_B200_OK;
+    } catch (const ddm::InputError& e) {
+        g_last_error = e.what();
+        return DDM_B200_E_INPUT;
+    } catch (const ddm::PlanError& e) {
+        g_last_error = e.what();
+        return DDM_B200_E_PLAN;
+    } catch (const ddm::IoError& e) {
+        g_last_error = e.what();
+        return DDM_B200_E_IO;
+    } catch (const ddm::DeviceError& e) {
+        g_last_error = e.what();
+        return DDM_B200_E_CUDA;
+    } catch (const ddm::b200::CudaError& e) {
+        g_last_error = e.what();
+        return DDM_B200_E_CUDA;
+    } catch (const std::bad_alloc& e) {
+        g_last_error = "out of host memory";
+        return DDM_B200_E_PLAN;
+    } catch (const std::length_error& e) {
+        g_last_error = e.what();
+        return DDM_B200_E_PLAN;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return DDM_B200_E_INTERNAL;
+    } catch (...) {
+        g_last_error = "unknown error";
+        return DDM_B200_E_INTERNAL;
+    }
+}
+
+ddm::RunConfig to_config(const ddm_b200_run_config* c) {
+    if (!c) throw ddm::InputError("null run config");
+    ddm::RunConfig r;
+    r.algorithm = c->algorithm == 0 ? ddm::Algorithm::WithFt
+                  : c->algorithm == 1 ? ddm::Algorithm::WithoutFt
+                                      : ddm::Algorithm::Direct;
+    r.precision = c->precision == 0 ? ddm::Precision::F32 : ddm::Precision::F64;
+    if (c->lags && c->n_lags > 0) r.lags.assign(c->lags, c->lags + c->n_lags);
+    if (c->has_q_max) r.q_max = c->q_max;
+    r.memory_bytes = c->memory_bytes;
+    r.workers = c->workers;
+    if (c->out_dir && c->out_dir[0]) r.out_dir = c->out_dir;
+    if (c->before_merge) {
+        auto fn = c->before_merge;
+        void* user = c->before_merge_user;
+        r.before_merge = [fn, user](const std::filesystem::path& ws) { fn(ws.string().c_str(), user); };
+    }
+    r.device = c->device;
+    return r;
+}
+
+void emit(const ddm::ResultArchive& a, int64_t* out_lags, int64_t* out_n_lags,
+          ddm_b200_counters* counters, ddm_b200_timing* timing) {
+    if (out_lags) std::copy(a.map.lags.begin(), a.map.lags.end(), out_lags);
+    if (out_n_lags) *out_n_lags = int64_t(a.map.lags.size());
+    if (counters) {
+        counters->spatial_ffts = a.counters.spatial_ffts;
+        counters->temporal_ffts = a.counters.temporal_ffts;
+        counters->pairs = a.counters.pairs;
+    }
+    if (timing) {
+        timing->disk = a.timing.disk;
+        timing->step1 = a.timing.step1;
+        timing->step2 = a.timing.step2;
+        timing->merge = a.timing.merge;
+        timing->other = a.timing.other;
+        timing->total = a.timing.total;
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ddm_b200_last_error(void) { return g_last_error.c_str(); }
+
+int ddm_b200_version(int* major, int* minor, int* patch) {
+    if (major) *major = 0;
+    if (minor) *minor = 1;
+    if (patch) *patch = 0;
+    return DDM_B200_OK;
+}
+
+int ddm_b200_device_count(int* count) {
+    return guarded([&] {
+        int n = 0;
+        const cudaError_t e = cudaGetDeviceCount(&n);
+        if (e != cudaSuccess) n = 0;
+        *count = n;
+    });
+}
+
+int64_t ddm_b200_pad_length(int64_t n) {
+    if (n < 1) return -1;
+    return ddm::pad_length(n);
+}
+
+int64_t ddm_b200_max_frames(int precision) { return ddm::b200::max_frames(precision != 0); }
+
+int ddm_b200_plan_with_ft(int64_t q_count, int64_t frames, int64_t bytes, int precision,
+                          int64_t* capacity, int64_t* groups) {
+    return guarded([&] {
+        const auto p = ddm::plan_with_ft(
+            q_count, frames, {bytes, precision == 0 ? ddm::Precision::F32 : ddm::Precision::F64});
+        *capacity = p.capacity;
+        *groups = p.group_count();
+    });
+}
+
+int ddm_b200_cutoff_set(int width, int height, int has_q_max, double q_max, int64_t* count,
+                        int64_t* flat_out) {
+    return guarded([&] {
+        const auto s = ddm::cutoff_set(width, height,
+                                       has_q_max ? std::optional<double>(q_max) : std::nullopt);
+        *count = s.count();
+        if (flat_out)
+            for (int64_t k = 0; k < s.count(); ++k) flat_out[k] = s.flat(k);
+    });
+}
+
+int ddm_b200_run_u16(const uint16_t* pixels, int width, int height, int frames,
+                     double frame_interval, const ddm_b200_run_config* config, double* out_values,
+                     int64_t out_capacity, int64_t* out_lags, int64_t* out_n_lags,
+                     ddm_b200_counters* counters, ddm_b200_timing* timing) {
+    return guarded([&] {
+        if (!pixels || !out_values) throw ddm::InputError("null pixel or output buffer");
+        ddm::ViewFrameSource src(pixels, width, height, frames, frame_interval);
+        const auto a = ddm::run_into(src, to_config(config), out_values, out_capacity);
+        emit(a, out_lags, out_n_lags, counters, timing);
+    });
+}
+
+int ddm_b200_run_u8(const uint8_t* pixels, int width, int height, int frames, double frame_interval,
+                    const ddm_b200_run_config* config, double* out_values, int64_t out_capacity,
+                    int64_t* out_lags, int64_t* out_n_lags, ddm_b200_counters* counters,
+                    ddm_b200_timing* timing) {
+    return guarded([&] {
+        if (!pixels || !out_values) throw ddm::InputError("null pixel or output buffer");
+        ddm::detail::Ingest in;
+        in.u8 = pixels;
+        in.width = width;
+        in.height = height;
+        in.frames = frames;
+        in.frame_interval = frame_interval;
+        const auto cfg = to_config(config);
+        const auto a = ddm::detail::guard_device(
+            [&] { return ddm::detail::run_core(in, cfg, out_values, out_capacity); });
+        emit(a, out_lags, out_n_lags, counters, timing);
+    });
+}
+
+int ddm_b200_run_raw_stack(const char* path, const ddm_b200_run_config* config, double* out_values,
+                           int64_t out_capacity, int64_t* out_lags, int64_t* out_n_lags,
+                           ddm_b200_counters* counters, ddm_b200_timing* timing) {
+    return guarded([&] {
+        if (!path) throw ddm::InputError("null path");
+        ddm::RawStackFileSource src(path);
+        const auto a = ddm::run_into(src, to_config(config), out_values, out_capacity);
+        emit(a, out_lags, out_n_lags, counters, timing);
+    });
+}
+
+int ddm_b200_run_device(const void* d_frames, int pixel_bytes, int width, int height, int frames,
+                        int precision, const int64_t* lags, int64_t n_lags, int has_q_max,
+                        double q_max, void* d_out, int out_f64, int device, void* stream,
+                        double* spatial_ms, double* temporal_ms, int* kernel_launches) {
+    return guarded([&] {
+        if (!d_frames || !d_out) throw ddm::InputError("null device buffer");
+        if (pixel_bytes != 1 && pixel_bytes != 2) throw ddm::InputError("pixel_bytes must be 1 or 2");
+        if (width < 1 || height < 1 || frames < 1) throw ddm::InputError("dimensions must be positive");
+        const bool f64 = precision != 0;
+        if (frames > ddm::b200::max_frames(f64))
+            throw ddm::PlanError("sequence longer than the device temporal engine limit");
+        std::vector<int64_t> lag_list = (lags && n_lags > 0)
+                                            ? ddm::normalize_lags({lags, lags + n_lags}, frames)
+                                            : ddm::all_lags(frames);
+        const auto wv = ddm::cutoff_set(width, height,
+                                        has_q_max ? std::optional<double>(q_max) : std::nullopt);
+        if (wv.count() < 1) throw ddm::InputError("wave-vector cutoff retains nothing");
+        ddm::detail::guard_device([&] {
+            auto& eng = ddm::b200::Engine::instance(device);
+            std::lock_guard<std::mutex> lock(eng.mutex());
+            cudaStream_t user = static_cast<cudaStream_t>(stream);
+            cudaEvent_t ev;
+            ddm::b200::check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+            ddm::b200::check(cudaEventRecord(ev, user), "event record");
+            ddm::b200::check(cudaStreamWaitEvent(eng.stream(), ev, 0), "stream wait");
+            ddm::b200::RunSpec sp;
+            sp.W = width;
+            sp.H = height;
+            sp.N = frames;
+            sp.f64 = f64;
+            sp.pixel_bytes = pixel_bytes;
+            sp.d_frames = d_frames;
+            sp.lags = lag_list;
+            sp.flat.resize(size_t(wv.count()));
+            sp.identity = true;
+            for (int64_t k = 0; k < wv.count(); ++k) {
+                sp.flat[size_t(k)] = wv.flat(k);
+                if (sp.flat[size_t(k)] != k) sp.identity = false;
+            }
+            sp.groups = {{0, wv.count()}};
+            sp.d_out = d_out;
+            sp.out_f64 = out_f64 != 0;
+            sp.out_stride = int64_t(height) * (width / 2 + 1);
+            ddm::b200::PhaseTimes t;
+            eng.run(sp, (spatial_ms || temporal_ms || kernel_launches) ? &t : nullptr);
+            ddm::b200::check(cudaEventRecord(ev, eng.stream()), "event record");
+            ddm::b200::check(cudaStreamWaitEvent(user, ev, 0), "stream wait");
+            cudaEventDestroy(ev);
+            if (spatial_ms) *spatial_ms = t.spatial_ms;
+            if (temporal_ms) *temporal_ms = t.temporal_ms;
+            if (kernel_launches) *kernel_launches = t.spatial_launches + t.temporal_launches;
+            return 0;
+        });
+    });
+}
+
+int ddm_b200_sequences_with_ft(const double* seq, int64_t q, int64_t n, int precision, int device,
+                               double* d, double* d_a, double* corr, uint64_t* temporal_ffts) {
+    return guarded([&] {
+        if (!seq || !d) throw ddm::InputError("null buffer");
+        if (q < 1 || n < 1) throw ddm::InputError("need at least one sequence of one value");
+        const bool f64 = precision != 0;
+        if (n > ddm::b200::max_frames(f64))
+            throw ddm::PlanError("sequence longer than the device temporal engine limit");
+        ddm::detail::guard_device([&] {
+            auto& eng = ddm::b200::Engine::instance(device);
+            std::lock_guard<std::mutex> lock(eng.mutex());
+            const size_t cnt = size_t(q) * size_t(n);
+            std::vector<unsigned char> host;
+            if (f64) {
+                host.resize(cnt * 16);
+                std::memcpy(host.data(), seq, cnt * 16);
+            } else {
+                host.resize(cnt * 8);
+                float* f = reinterpret_cast<float*>(host.data());
+                for (size_t i = 0; i < 2 * cnt; ++i) f[i] = float(seq[i]);
+            }
+            const size_t outs = cnt * sizeof(double);
+            char* dev = static_cast<char*>(eng.buffer("seq_io", host.size() + 3 * outs));
+            double* dd = reinterpret_cast<double*>(dev + host.size());
+            double* dda = dd + cnt;
+            double* dco = dda + cnt;
+            ddm::b200::check(cudaMemcpy(dev, host.data(), host.size(), cudaMemcpyHostToDevice), "upload");
+            eng.sequences(dev, q, n, f64, dd, d_a ? dda : nullptr, corr ? dco : nullptr);
+            ddm::b200::check(cudaMemcpy(d, dd, outs, cudaMemcpyDeviceToHost), "download");
+            if (d_a) ddm::b200::check(cudaMemcpy(d_a, dda, outs, cudaMemcpyDeviceToHost), "download");
+            if (corr) ddm::b200::check(cudaMemcpy(corr, dco, outs, cudaMemcpyDeviceToHost), "download");
+            return 0;
+        });
+        if (temporal_ffts) *temporal_ffts = 2 * uint64_t(q);
+    });
+}
+
+int ddm_b200_spectra_u16(const uint16_t* pixels, int width, int height, int frames, int precision,
+                         int device, double* out) {
+    return guarded([&] {
+        if (!pixels || !out) throw ddm::InputError("null buffer");
+        if (width < 1 || height < 1 || frames < 1) throw ddm::InputError("dimensions must be positive");
+        ddm::detail::guard_device([&] {
+            auto& eng = ddm::b200::Engine::instance(device);
+            std::lock_guard<std::mutex> lock(eng.mutex());
+            const bool f64 = precision != 0;
+            const size_t np = size_t(height) * (width / 2 + 1) * size_t(frames);
+            const size_t inb = (size_t(width) * height * frames * 2 + 255) / 256 * 256;
+            const size_t cs = f64 ? 16 : 8;
+            char* dev = static_cast<char*>(eng.buffer("spectra_io", inb + np * cs));
+            ddm::b200::check(cudaMemcpy(dev, pixels, size_t(width) * height * frames * 2, cudaMemcpyHostToDevice), "upload");
+            eng.spectra(dev, 2, width, height, frames, f64, dev + inb);
+            if (f64) {
+                ddm::b200::check(cudaMemcpy(out, dev + inb, np * 16, cudaMemcpyDeviceToHost), "download");
+            } else {
+                std::vector<float> tmp(2 * np);
+                ddm::b200::check(cudaMemcpy(tmp.data(), dev + inb, np * 8, cudaMemcpyDeviceToHost), "download");
+                for (size_t i = 0; i < 2 * np; ++i) out[i] = tmp[i];
+            }
+            return 0;
+        });
+    });
+}
+
+int ddm_b200_forward_spectrum(const double* frame, int width, int height, int precision, int device,
+                              double* out) {
+    (void)device;
+    return guarded([&] {
+        if (!frame || !out) throw ddm::InputError("null buffer");
+        const size_t n = size_t(width) * size_t(height);
+        if (precision != 0) {
+            const auto s = ddm::forward_spectrum<double>({frame, n}, width, height);
+            std::memcpy(out, s.data(), s.size() * sizeof(s[0]));
+        } else {
+            std::vector<float> f(frame, frame + n);
+            const auto s = ddm::forward_spectrum<float>({f.data(), n}, width, height);
+            for (size_t i = 0; i < s.size(); ++i) {
+                out[2 * i] = s[i].real();
+                out[2 * i + 1] = s[i].imag();
+            }
+        }
+    });
+}
+
+int ddm_b200_azimuthal(const double* values, int64_t n_lags, int width, int height, int has_q_max,
+                       double q_max, int device, double* means, int64_t* counts, int64_t capacity,
+                       int64_t* bin_count) {
+    (void)device;
+    return guarded([&] {
+        ddm::ResultMap map;
+        map.width = width;
+        map.height = height;
+        map.lags.resize(size_t(n_lags));
+        for (int64_t i = 0; i < n_lags; ++i) map.lags[size_t(i)] = i;
+        map.values.assign(values, values + size_t(map.plane_size() * n_lags));
+        const auto wv = ddm::cutoff_set(width, height,
+                                        has_q_max ? std::optional<double>(q_max) : std::nullopt);
+        const auto p = ddm::azimuthal_average(map, wv);
+        *bin_count = p.bin_count;
+        if (p.bin_count > capacity) throw ddm::InputError("bin capacity too small");
+        std::copy(p.counts.begin(), p.counts.end(), counts);
+        std::copy(p.means.begin(), p.means.end(), means);
+    });
+}
+
+int ddm_b200_generate(int64_t particles, double diffusion, double psf_sigma, double amplitude,
+                      double background, int width, int height, int frames, double frame_interval,
+                      uint64_t seed, uint16_t* out) {
+    return guarded([&] {
+        ddm::SynthConfig c;
+        c.particles = particles;
+        c.diffusion = diffusion;
+        c.psf_sigma = psf_sigma;
+        c.amplitude = amplitude;
+        c.background = background;
+        c.width = width;
+        c.height = height;
+        c.frames = frames;
+        c.frame_interval = frame_interval;
+        c.seed = seed;
+        const auto st = ddm::generate(c);
+        std::copy(st.pixels.begin(), st.pixels.end(), out);
+    });
+}
+
+}  // extern "C"

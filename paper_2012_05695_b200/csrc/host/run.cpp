@@ -1,0 +1,328 @@
+// ddm::run on the GPU (reference `proj/core/src/scheduler.cpp:413-483` + `run_with_ft`
+// `:62-180` + `merge_partials` `:485-542`).
+//
+// What stays the reference's: validation and error taxonomy, lag normalisation, the
+// wave-vector cutoff list, the budget floor and group plan from `memory_bytes`, the exact
+// counters (spatial_ffts = N x groups, temporal_ffts = 2 Q), the partial-file workspace
+// with `before_merge`, d(0) = 0, the lag-major f64 map and `validate()`.
+// What changes: frames are staged to HBM once (a contiguous source is one DMA); each group
+// is one batched spatial pass + one temporal launch on the device (engine.cu); without an
+// out_dir / before_merge seam the map is written in place on the device and copied back
+// once, instead of the partial write + re-read + scatter the reference always performs.
+#include "ddm/errors.hpp"
+#include "ddm/scheduler.hpp"
+#include "ddm/spectrum.hpp"
+#include "ddm/temporal.hpp"
+#include "run_internal.hpp"
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstring>
+
+#include <unistd.h>
+
+namespace fs = std::filesystem;
+
+namespace ddm {
+
+namespace {
+
+struct TempWorkspace {
+    fs::path path;
+    bool active = false;
+    ~TempWorkspace() {
+        if (active) {
+            std::error_code ec;
+            fs::remove_all(path, ec);
+        }
+    }
+};
+
+fs::path make_temp_dir() {
+    static std::atomic<std::uint64_t> counter{0};
+    const auto base = fs::temp_directory_path();
+    for (;;) {
+        const auto p = base / ("ddm-b200-run-" + std::to_string(::getpid()) + "-" +
+                               std::to_string(counter.fetch_add(1)));
+        std::error_code ec;
+        if (fs::create_directory(p, ec)) return p;
+        if (ec) throw IoError("cannot create temp workspace " + p.string());
+    }
+}
+
+// Frames -> device buffer of the engine. A contiguous u16/u8 source is one copy; otherwise
+// frames are read through the FrameSource interface into pinned staging, double buffered.
+const void* stage_frames(b200::Engine& eng, const detail::Ingest& in, double& disk_s) {
+    const auto t0 = std::chrono::steady_clock::now();
+    const std::size_t ppf = std::size_t(in.width) * in.height;
+    const std::size_t pb = in.u8 ? 1 : 2;
+    void* d = eng.frame_buffer(ppf * pb * std::size_t(in.frames));
+    cudaStream_t st = eng.stream();
+    if (in.u8 || (in.source && in.source->contiguous())) {
+        const void* src = in.u8 ? static_cast<const void*>(in.u8)
+                                : static_cast<const void*>(in.source->contiguous());
+        b200::check(cudaMemcpyAsync(d, src, ppf * pb * std::size_t(in.frames),
+                                    cudaMemcpyHostToDevice, st), "frame upload");
+        b200::check(cudaStreamSynchronize(st), "sync");
+    } else {
+        const int chunk = int(std::max<std::size_t>(1, std::min<std::size_t>(
+                                  std::size_t(in.frames), (32u << 20) / (ppf * 2))));
+        std::uint16_t* pinned[2] = {nullptr, nullptr};
+        cudaEvent_t done[2];
+        for (int i = 0; i < 2; ++i) {
+            b200::check(cudaMallocHost(reinterpret_cast<void**>(&pinned[i]), ppf * 2 * chunk),
+                        "cudaMallocHost");
+            b200::check(cudaEventCreate(&done[i]), "cudaEventCreate");
+        }
+        int slot = 0;
+        bool used[2] = {false, false};
+        try {
+            for (int f0 = 0; f0 < in.frames; f0 += chunk) {
+                const int nf = std::min(chunk, in.frames - f0);
+                if (used[slot]) b200::check(cudaEventSynchronize(done[slot]), "sync");
+                for (int i = 0; i < nf; ++i)
+                    in.source->read_frame(f0 + i, {pinned[slot] + std::size_t(i) * ppf, ppf});
+                b200::check(cudaMemcpyAsync(static_cast<std::uint16_t*>(d) + std::size_t(f0) * ppf,
+                                            pinned[slot], ppf * 2 * nf, cudaMemcpyHostToDevice, st),
+                            "frame upload");
+                b200::check(cudaEventRecord(done[slot], st), "cudaEventRecord");
+                used[slot] = true;
+                slot ^= 1;
+            }
+            b200::check(cudaStreamSynchronize(st), "sync");
+        } catch (...) {
+            cudaStreamSynchronize(st);
+            for (int i = 0; i < 2; ++i) {
+                cudaFreeHost(pinned[i]);
+                cudaEventDestroy(done[i]);
+            }
+            throw;
+        }
+        for (int i = 0; i < 2; ++i) {
+            cudaFreeHost(pinned[i]);
+            cudaEventDestroy(done[i]);
+        }
+    }
+    disk_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return d;
+}
+
+}  // namespace
+
+namespace detail {
+
+ResultArchive run_core(const Ingest& in, const RunConfig& config, double* out,
+                       std::int64_t capacity) {
+    const auto wall0 = std::chrono::steady_clock::now();
+    if (config.workers < 1) throw InputError("workers must be at least 1");
+    if (in.frames < 1) throw InputError("stack has no frames");
+    if (in.width < 1 || in.height < 1) throw InputError("frame dimensions must be positive");
+    if (config.algorithm != Algorithm::WithFt)
+        throw InputError("algorithm '" + to_string(config.algorithm) +
+                         "' is not part of the b200 accelerated path (with_ft only)");
+    const int W = in.width, H = in.height, N = in.frames;
+    const std::vector<std::int64_t> lags =
+        config.lags.empty() ? all_lags(N) : normalize_lags(config.lags, N);
+    if (lags.empty()) throw InputError("no lags");
+    const WaveVectorSet wv = cutoff_set(W, H, config.q_max);
+    if (wv.count() < 1) throw InputError("wave-vector cutoff retains nothing");
+
+    ResultArchive archive;
+    archive.frames = N;
+    archive.algorithm = to_string(config.algorithm);
+    archive.precision = to_string(config.precision);
+    archive.q_max = config.q_max;
+    archive.workers = config.workers;
+    archive.map.width = W;
+    archive.map.height = H;
+    archive.map.frame_interval = in.frame_interval;
+    archive.map.lags = lags;
+    const std::int64_t plane = archive.map.plane_size();
+    const std::int64_t total = plane * std::int64_t(lags.size());
+    if (capacity < total) throw InputError("output capacity is smaller than lags x plane");
+
+    // budget floor + group plan (`scheduler.cpp:73-84`, `:365-384`)
+    const MemoryBudget budget{config.memory_bytes, config.precision};
+    const std::int64_t floor_bytes =
+        spectrum_bytes(W, H, config.precision) + pad_length(N) * budget.complex_size();
+    if (budget.bytes < floor_bytes)
+        throw PlanError("memory budget " + std::to_string(budget.bytes) +
+                        " bytes is below the working minimum of " + std::to_string(floor_bytes) +
+                        " bytes");
+    const GroupPlan plan = plan_with_ft(wv.count(), N, budget);
+    const bool f64 = config.precision == Precision::F64;
+    if (N > b200::max_frames(f64))
+        throw PlanError("sequence of " + std::to_string(N) + " frames exceeds the device temporal "
+                        "engine limit of " + std::to_string(b200::max_frames(f64)) + " (" +
+                        to_string(config.precision) + ")");
+
+    TimingBreakdown timing;
+    b200::Engine& eng = b200::Engine::instance(config.device);
+    std::lock_guard<std::mutex> lock(eng.mutex());
+    cudaStream_t st = eng.stream();
+
+    const void* d_frames = stage_frames(eng, in, timing.disk);
+
+    b200::RunSpec spec;
+    spec.W = W;
+    spec.H = H;
+    spec.N = N;
+    spec.f64 = f64;
+    spec.pixel_bytes = in.u8 ? 1 : 2;
+    spec.d_frames = d_frames;
+    spec.lags = lags;
+    spec.identity = !config.q_max.has_value() || wv.count() == plane;
+    spec.flat.resize(std::size_t(wv.count()));
+    for (std::int64_t k = 0; k < wv.count(); ++k) spec.flat[std::size_t(k)] = wv.flat(k);
+    if (spec.identity)
+        for (std::int64_t k = 0; k < wv.count(); ++k)
+            if (spec.flat[std::size_t(k)] != k) spec.identity = false;
+    spec.groups = plan.groups;
+    spec.out_f64 = true;
+    spec.out_stride = plane;
+
+    const bool keep_partials = !config.out_dir.empty() || bool(config.before_merge);
+    TempWorkspace temp;
+    fs::path workspace = config.out_dir;
+    b200::PhaseTimes times;
+    PhaseClock clock;
+
+    if (keep_partials) {
+        if (workspace.empty()) {
+            workspace = make_temp_dir();
+            temp.path = workspace;
+            temp.active = true;
+        } else {
+            std::error_code ec;
+            fs::create_directories(workspace, ec);
+            if (ec) throw IoError("cannot create workspace " + workspace.string());
+        }
+        spec.partial_mode = true;
+        std::vector<double> host;
+        spec.on_partial = [&](std::size_t g, const void* d_partial, std::int64_t gc) {
+            clock.start();
+            PartialResult p;
+            p.group = std::int64_t(g);
+            p.wv_begin = plan.groups[g].first;
+            p.wv_end = plan.groups[g].second;
+            p.width = W;
+            p.height = H;
+            p.frames = N;
+            p.frame_interval = in.frame_interval;
+            p.q_max = config.q_max;
+            p.lags = lags;
+            p.values.resize(lags.size() * std::size_t(gc));
+            b200::check(cudaMemcpyAsync(p.values.data(), d_partial, p.values.size() * sizeof(double),
+                                        cudaMemcpyDeviceToHost, st), "partial copy");
+            b200::check(cudaStreamSynchronize(st), "sync");
+            write_partial(p, workspace);
+            clock.stop(timing.merge);
+        };
+        eng.run(spec, &times);
+        if (config.before_merge) config.before_merge(workspace);
+        clock.start();
+        const ResultMap merged = merge_partials(list_partials(workspace));
+        if (merged.lags != lags || std::int64_t(merged.values.size()) != total)
+            throw InputError("merged partials do not match the run layout");
+        std::memcpy(out, merged.values.data(), std::size_t(total) * sizeof(double));
+        clock.stop(timing.merge);
+        archive.map.values.clear();
+    } else {
+        double* d_map = static_cast<double*>(eng.buffer("map", std::size_t(total) * sizeof(double)));
+        if (!spec.identity)
+            b200::check(cudaMemsetAsync(d_map, 0, std::size_t(total) * sizeof(double), st), "memset");
+        spec.d_out = d_map;
+        eng.run(spec, &times);
+        // validate on the device before the copy (`archive.cpp:44-58`)
+        bool finite = true;
+        double peak = 0.0, lowest = 0.0;
+        b200::reduce_stats(d_map, total, st, &finite, &peak, &lowest);
+        if (!finite) throw InputError("result map contains non-finite values");
+        const double eps = f64 ? 1e-9 : 1e-4;
+        if (lowest < -eps * std::max(peak, 1.0))
+            throw InputError("result map contains negative values beyond tolerance");
+        clock.start();
+        b200::check(cudaMemcpyAsync(out, d_map, std::size_t(total) * sizeof(double),
+                                    cudaMemcpyDeviceToHost, st), "map copy");
+        b200::check(cudaStreamSynchronize(st), "sync");
+        clock.stop(timing.merge);
+    }
+    timing.step1 = times.spatial_ms * 1e-3;
+    timing.step2 = times.temporal_ms * 1e-3;
+    archive.counters.spatial_ffts = std::uint64_t(N) * std::uint64_t(plan.group_count());
+    archive.counters.temporal_ffts = 2 * std::uint64_t(wv.count());
+    timing.finish(std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count());
+    archive.timing = timing;
+    return archive;
+}
+
+}  // namespace detail
+
+ResultArchive run_into(FrameSource& source, const RunConfig& config, double* out,
+                       std::int64_t capacity) {
+    detail::Ingest in;
+    in.source = &source;
+    in.width = source.width();
+    in.height = source.height();
+    in.frames = source.frames();
+    in.frame_interval = source.frame_interval();
+    return detail::guard_device([&] { return detail::run_core(in, config, out, capacity); });
+}
+
+ResultArchive run(FrameSource& source, const RunConfig& config) {
+    if (source.frames() < 1) throw InputError("stack has no frames");
+    if (config.workers < 1) throw InputError("workers must be at least 1");
+    const std::int64_t n_lags =
+        config.lags.empty() ? source.frames() : std::int64_t(config.lags.size());
+    std::vector<double> values(std::size_t(n_lags) * std::size_t(source.height()) *
+                               std::size_t(half_cols(source.width())));
+    ResultArchive a = run_into(source, config, values.data(), std::int64_t(values.size()));
+    values.resize(std::size_t(a.map.plane_size()) * a.map.lags.size());
+    a.map.values = std::move(values);
+    return a;
+}
+
+ResultMap merge_partials(const std::vector<fs::path>& files) {
+    if (files.empty()) throw InputError("no partial files to merge");
+    std::vector<PartialResult> parts;
+    parts.reserve(files.size());
+    for (const auto& f : files) parts.push_back(read_partial(f));
+    const PartialResult& first = parts.front();
+    for (const auto& p : parts)
+        if (p.width != first.width || p.height != first.height || p.frames != first.frames ||
+            p.frame_interval != first.frame_interval || p.q_max != first.q_max || p.lags != first.lags)
+            throw InputError("partial files disagree on geometry or lags");
+    std::sort(parts.begin(), parts.end(),
+              [](const PartialResult& a, const PartialResult& b) { return a.wv_begin < b.wv_begin; });
+    const WaveVectorSet wv = cutoff_set(int(first.width), int(first.height), first.q_max);
+    std::int64_t cursor = 0;
+    for (const auto& p : parts) {
+        if (p.wv_begin < cursor)
+            throw InputError("partial files overlap at wave vector " + std::to_string(p.wv_begin));
+        if (p.wv_begin > cursor)
+            throw InputError("partial files leave a gap before wave vector " + std::to_string(p.wv_begin));
+        cursor = p.wv_end;
+    }
+    if (cursor != wv.count())
+        throw InputError("partial files cover " + std::to_string(cursor) + " of " +
+                         std::to_string(wv.count()) + " wave vectors");
+    ResultMap map;
+    map.width = first.width;
+    map.height = first.height;
+    map.frame_interval = first.frame_interval;
+    map.lags = first.lags;
+    map.values.assign(std::size_t(map.plane_size()) * map.lags.size(), 0.0);
+    for (const auto& p : parts) {
+        const auto cnt = std::size_t(p.wv_count());
+        for (std::size_t li = 0; li < p.lags.size(); ++li) {
+            auto plane = map.lag_plane(std::int64_t(li));
+            const double* src = p.values.data() + li * cnt;
+            for (std::size_t j = 0; j < cnt; ++j)
+                plane[std::size_t(wv.flat(p.wv_begin + std::int64_t(j)))] = src[j];
+        }
+    }
+    return map;
+}
+
+}  // namespace ddm

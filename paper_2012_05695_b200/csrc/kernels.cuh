@@ -1,0 +1,70 @@
+// Launch interface of the DDM device kernels (spatial r2c + corner turn, temporal engine).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "fft_core.cuh"
+
+namespace ddmk {
+
+// Twiddle table tw[j] = exp(-2 pi i j / len), j < len, in the working precision.
+struct TwTable {
+    int len = 0;
+    const void* ptr = nullptr;  // cpx<S>*
+};
+
+// Spectra layout on device ("tile-major corner turn"): the retained wave vectors of one
+// group, slots s in [0, g_count), are cut into tiles of T consecutive slots and stored
+//     spec[((s / T) * N + n) * T + (s % T)]        (complex, working precision)
+// so one tile is a contiguous N x T block: the spatial kernel writes T-wide runs per
+// frame, the temporal kernel streams a whole tile as one contiguous block.
+struct SpecLayout {
+    int T = 4;
+    int64_t g_begin = 0;   // first retained index of the group
+    int64_t g_count = 0;   // slots in the group
+    int64_t tiles() const { return (g_count + T - 1) / T; }
+};
+
+struct SpatialArgs {
+    const void* frames = nullptr;  // [N][H][W] pixels
+    int pixel_bytes = 2;           // 2 u16, 1 u8, 4 f32, 8 f64 (real-valued frames)
+    int W = 0, H = 0, N = 0;
+    int frame0 = 0, nframes = 0;   // chunk of frames to transform
+    void* mid = nullptr;           // [chunk frame][W/2+1][H] complex scratch
+    void* spec = nullptr;
+    SpecLayout layout;
+    const int* slot_of_flat = nullptr;  // nullable: flat (row*(W/2+1)+col) -> retained index
+    TwTable tw_row, tw_post, tw_col;    // row (W/2 or W), post (W), column (H)
+};
+
+struct TemporalArgs {
+    const void* spec = nullptr;
+    int N = 0, N2 = 0;
+    SpecLayout layout;
+    TwTable tw;                        // length N2
+    TwTable tw_half;                   // length N2 / 2
+    const int* lag_index = nullptr;    // [N] -> output lag slot or -1
+    void* out = nullptr;               // out[li * out_stride + dest(s)]
+    int out_f64 = 1;
+    int64_t out_stride = 0;
+    const int64_t* dest_of_slot = nullptr;  // nullable: slot -> destination column
+    // optional diagnostics for the batched SequenceEngine API: corr in the shifted basis,
+    // f64 [slot][N], and the per-slot mean (complex f64) used for the restore
+    double* corr_out = nullptr;
+    double* mean_out = nullptr;
+};
+
+template <typename S>
+cudaError_t launch_spatial(const SpatialArgs& a, cudaStream_t stream);
+
+template <typename S>
+cudaError_t launch_temporal(const TemporalArgs& a, cudaStream_t stream);
+
+// Shared memory / tile geometry chosen for the temporal kernel; the spectra layout T must
+// match it. Returns 0 when the sequence length is beyond what one CTA can hold.
+int temporal_tile(int N, int N2, int scalar_bytes);
+size_t temporal_smem_bytes(int N, int N2, int T, int scalar_bytes);
+int temporal_threads(int N2, int T);
+
+}  // namespace ddmk

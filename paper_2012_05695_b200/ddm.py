@@ -1,0 +1,360 @@
+"""Python view of the ddm-b200 C-ABI (include/ddm_b200.h), mirroring the reference API.
+
+Names and argument meaning follow the reference C++ library (`proj/core/include/ddm/*.hpp`):
+`run(stack, RunConfig)` is `ddm::run` over a MemoryFrameSource, `with_ft_sequence` is the
+per-sequence engine, errors are `InputError` / `PlanError` / `IoError` (plus `DeviceError`).
+All compute happens in `libddm_b200.so` on the GPU; there is no CPU fallback — if the
+library is missing this module raises on first use.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from pathlib import Path
+from typing import Callable, Optional, Sequence
+
+import numpy as np
+
+LIB_PATH = Path(__file__).resolve().parent / "libddm_b200.so"
+
+
+class Error(RuntimeError):
+    """ddm::Error"""
+
+
+class InputError(Error):
+    """ddm::InputError (status 1)"""
+
+
+class PlanError(Error):
+    """ddm::PlanError (status 2)"""
+
+
+class IoError(Error):
+    """ddm::IoError (status 3)"""
+
+
+class DeviceError(Error):
+    """device failure (status 4)"""
+
+
+_ERR = {1: InputError, 2: PlanError, 3: IoError, 4: DeviceError, 5: Error}
+
+
+class Counters(C.Structure):
+    _fields_ = [("spatial_ffts", C.c_uint64), ("temporal_ffts", C.c_uint64), ("pairs", C.c_uint64)]
+
+
+class Timing(C.Structure):
+    _fields_ = [(k, C.c_double) for k in ("disk", "step1", "step2", "merge", "other", "total")]
+
+
+BEFORE_MERGE = C.CFUNCTYPE(None, C.c_char_p, C.c_void_p)
+
+
+class _RunConfig(C.Structure):
+    _fields_ = [("algorithm", C.c_int), ("precision", C.c_int), ("lags", C.POINTER(C.c_int64)),
+                ("n_lags", C.c_int64), ("has_q_max", C.c_int), ("q_max", C.c_double),
+                ("memory_bytes", C.c_int64), ("workers", C.c_int), ("out_dir", C.c_char_p),
+                ("before_merge", BEFORE_MERGE), ("before_merge_user", C.c_void_p),
+                ("device", C.c_int)]
+
+
+_lib = None
+
+
+def lib():
+    """Load the native library (raises if it was not built — no silent fallback)."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2012_05695_b200.build`")
+        L = C.CDLL(str(LIB_PATH))
+        L.ddm_b200_last_error.restype = C.c_char_p
+        L.ddm_b200_pad_length.restype = C.c_int64
+        L.ddm_b200_pad_length.argtypes = [C.c_int64]
+        L.ddm_b200_max_frames.restype = C.c_int64
+        L.ddm_b200_max_frames.argtypes = [C.c_int]
+        L.ddm_b200_run_device.argtypes = [
+            C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int64),
+            C.c_int64, C.c_int, C.c_double, C.c_void_p, C.c_int, C.c_int, C.c_void_p,
+            C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_int)]
+        _lib = L
+    return _lib
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        msg = lib().ddm_b200_last_error().decode(errors="replace")
+        raise _ERR.get(rc, Error)(msg)
+
+
+def _p(a, ct):
+    return a.ctypes.data_as(C.POINTER(ct))
+
+
+def device_count() -> int:
+    n = C.c_int(0)
+    _check(lib().ddm_b200_device_count(C.byref(n)))
+    return n.value
+
+
+def pad_length(n: int) -> int:
+    v = lib().ddm_b200_pad_length(n)
+    if v < 0:
+        raise InputError("pad_length: sequence must have at least one frame")
+    return int(v)
+
+
+def max_frames(precision: str = "f32") -> int:
+    return int(lib().ddm_b200_max_frames(0 if precision == "f32" else 1))
+
+
+def half_cols(width: int) -> int:
+    return width // 2 + 1
+
+
+def plan_with_ft(q_count: int, frames: int, nbytes: int, precision: str = "f64"):
+    cap, groups = C.c_int64(0), C.c_int64(0)
+    _check(lib().ddm_b200_plan_with_ft(C.c_int64(q_count), C.c_int64(frames), C.c_int64(nbytes),
+                                       0 if precision == "f32" else 1, C.byref(cap), C.byref(groups)))
+    return int(cap.value), int(groups.value)
+
+
+def cutoff_set(width: int, height: int, q_max: Optional[float] = None) -> np.ndarray:
+    count = C.c_int64(0)
+    has, qm = (0, 0.0) if q_max is None else (1, float(q_max))
+    _check(lib().ddm_b200_cutoff_set(width, height, has, C.c_double(qm), C.byref(count), None))
+    flat = np.zeros(count.value, dtype=np.int64)
+    _check(lib().ddm_b200_cutoff_set(width, height, has, C.c_double(qm), C.byref(count),
+                                     _p(flat, C.c_int64)))
+    return flat
+
+
+@dataclass
+class RunConfig:
+    """ddm::RunConfig (`scheduler.hpp:78-93`)."""
+    algorithm: str = "with_ft"
+    precision: str = "f64"
+    lags: Sequence[int] = ()
+    q_max: Optional[float] = None
+    memory_bytes: int = 0
+    workers: int = 2
+    out_dir: Optional[str] = None
+    before_merge: Optional[Callable[[str], None]] = None
+    device: int = 0
+
+
+@dataclass
+class ResultArchive:
+    """ddm::ResultArchive: map values lag-major [lags, H, W/2+1] f64."""
+    values: np.ndarray
+    lags: np.ndarray
+    width: int
+    height: int
+    frames: int
+    frame_interval: float
+    algorithm: str
+    precision: str
+    q_max: Optional[float]
+    workers: int
+    counters: dict = field(default_factory=dict)
+    timing: dict = field(default_factory=dict)
+
+    def lag_plane(self, i: int) -> np.ndarray:
+        return self.values[i]
+
+    def lag_index(self, lag: int) -> int:
+        idx = np.searchsorted(self.lags, lag)
+        return int(idx) if idx < len(self.lags) and self.lags[idx] == lag else -1
+
+
+def _config(cfg: RunConfig, keep):
+    alg = {"with_ft": 0, "without_ft": 1, "direct": 2}.get(cfg.algorithm)
+    if alg is None:
+        raise InputError(f"unknown algorithm '{cfg.algorithm}'")
+    if cfg.precision not in ("f32", "f64"):
+        raise InputError(f"unknown precision '{cfg.precision}'")
+    lags = np.ascontiguousarray(np.asarray(list(cfg.lags), dtype=np.int64))
+    keep.append(lags)
+    c = _RunConfig()
+    c.algorithm = alg
+    c.precision = 0 if cfg.precision == "f32" else 1
+    c.lags = _p(lags, C.c_int64) if len(lags) else None
+    c.n_lags = len(lags)
+    c.has_q_max = 0 if cfg.q_max is None else 1
+    c.q_max = 0.0 if cfg.q_max is None else float(cfg.q_max)
+    c.memory_bytes = int(cfg.memory_bytes)
+    c.workers = int(cfg.workers)
+    c.out_dir = cfg.out_dir.encode() if cfg.out_dir else None
+    if cfg.before_merge is not None:
+        user_fn = cfg.before_merge
+        errors = []
+
+        def tramp(ws, _user):
+            try:
+                user_fn(ws.decode())
+            except Exception as e:  # pragma: no cover - surfaced below
+                errors.append(e)
+        cb = BEFORE_MERGE(tramp)
+        keep.append(cb)
+        keep.append(errors)
+        c.before_merge = cb
+    else:
+        c.before_merge = BEFORE_MERGE()
+    c.before_merge_user = None
+    c.device = int(cfg.device)
+    return c
+
+
+def run(stack, config: RunConfig, frame_interval: float = 1.0) -> ResultArchive:
+    """ddm::run (`scheduler.cpp:413-483`) on a frame-major [N, H, W] uint16 (or uint8) stack."""
+    st = np.asarray(stack)
+    if st.ndim != 3:
+        raise InputError("stack must be [frames, height, width]")
+    u8 = st.dtype == np.uint8
+    st = np.ascontiguousarray(st, dtype=np.uint8 if u8 else np.uint16)
+    n, h, w = st.shape
+    n_out = len(config.lags) if len(config.lags) else n
+    plane = h * half_cols(w)
+    values = np.empty(max(n_out, 1) * plane)
+    out_lags = np.zeros(max(n_out, 1), dtype=np.int64)
+    n_lags = C.c_int64(0)
+    counters, timing = Counters(), Timing()
+    keep: list = []
+    c = _config(config, keep)
+    fn = lib().ddm_b200_run_u8 if u8 else lib().ddm_b200_run_u16
+    rc = fn(_p(st, C.c_uint8 if u8 else C.c_uint16), w, h, n, C.c_double(frame_interval),
+            C.byref(c), _p(values, C.c_double), C.c_int64(values.size), _p(out_lags, C.c_int64),
+            C.byref(n_lags), C.byref(counters), C.byref(timing))
+    for item in keep:
+        if isinstance(item, list) and item and isinstance(item[0], Exception):
+            raise item[0]
+    _check(rc)
+    k = n_lags.value
+    return ResultArchive(values[: k * plane].reshape(k, h, half_cols(w)), out_lags[:k].copy(), w, h,
+                         n, frame_interval, config.algorithm, config.precision, config.q_max,
+                         config.workers,
+                         {f: int(getattr(counters, f)) for f, _ in Counters._fields_},
+                         {f: float(getattr(timing, f)) for f, _ in Timing._fields_})
+
+
+def run_raw_stack(path: str, config: RunConfig) -> ResultArchive:
+    """ddm::run over a RawStackFileSource (`frame_source.cpp:27-78`)."""
+    with open(path, "rb") as f:
+        import json
+        hdr = json.loads(f.readline())
+    n, h, w = int(hdr["frames"]), int(hdr["height"]), int(hdr["width"])
+    n_out = len(config.lags) if len(config.lags) else n
+    plane = h * half_cols(w)
+    values = np.empty(max(n_out, 1) * plane)
+    out_lags = np.zeros(max(n_out, 1), dtype=np.int64)
+    n_lags = C.c_int64(0)
+    counters, timing = Counters(), Timing()
+    keep: list = []
+    c = _config(config, keep)
+    rc = lib().ddm_b200_run_raw_stack(str(path).encode(), C.byref(c), _p(values, C.c_double),
+                                      C.c_int64(values.size), _p(out_lags, C.c_int64),
+                                      C.byref(n_lags), C.byref(counters), C.byref(timing))
+    _check(rc)
+    k = n_lags.value
+    return ResultArchive(values[: k * plane].reshape(k, h, half_cols(w)), out_lags[:k].copy(), w, h,
+                         n, float(hdr.get("frame_interval", 1.0)), config.algorithm,
+                         config.precision, config.q_max, config.workers,
+                         {f: int(getattr(counters, f)) for f, _ in Counters._fields_},
+                         {f: float(getattr(timing, f)) for f, _ in Timing._fields_})
+
+
+@dataclass
+class LagProfile:
+    d: np.ndarray
+    d_a: np.ndarray
+    corr: np.ndarray
+
+
+def sequences_with_ft(seqs, precision: str = "f64", device: int = 0, terms: bool = False):
+    """Batched SequenceEngine<S>::with_ft on the GPU: seqs [Q, N] complex -> d [Q, N] (and
+    d_a, corr restored to the original basis when terms=True)."""
+    s = np.ascontiguousarray(np.atleast_2d(np.asarray(seqs, dtype=np.complex128)))
+    q, n = s.shape
+    d = np.empty((q, n))
+    d_a = np.empty((q, n)) if terms else None
+    corr = np.empty((q, n)) if terms else None
+    cnt = C.c_uint64(0)
+    _check(lib().ddm_b200_sequences_with_ft(
+        _p(s.view(np.float64), C.c_double), C.c_int64(q), C.c_int64(n),
+        0 if precision == "f32" else 1, device, _p(d, C.c_double),
+        _p(d_a, C.c_double) if terms else None, _p(corr, C.c_double) if terms else None,
+        C.byref(cnt)))
+    return (d, d_a, corr) if terms else d
+
+
+def with_ft_sequence(seq, precision: str = "f64") -> LagProfile:
+    """ddm::with_ft_sequence<S> (`temporal.cpp:141-148`)."""
+    d, d_a, corr = sequences_with_ft(np.asarray(seq)[None, :], precision, terms=True)
+    return LagProfile(d[0], d_a[0], corr[0])
+
+
+def compute_spectra(stack, precision: str = "f64", device: int = 0) -> np.ndarray:
+    """ddm::compute_spectra (`spectrum.cpp:29-63`): [N, H, W/2+1] complex128."""
+    st = np.ascontiguousarray(stack, dtype=np.uint16)
+    n, h, w = st.shape
+    out = np.empty((n, h, half_cols(w)), dtype=np.complex128)
+    _check(lib().ddm_b200_spectra_u16(_p(st, C.c_uint16), w, h, n, 0 if precision == "f32" else 1,
+                                      device, _p(out.view(np.float64), C.c_double)))
+    return out
+
+
+def forward_spectrum(frame, width: int, height: int, precision: str = "f64") -> np.ndarray:
+    """ddm::forward_spectrum (`spectrum.cpp:12-27`): [H, W/2+1] complex128."""
+    f = np.ascontiguousarray(np.asarray(frame, dtype=np.float64).reshape(-1))
+    out = np.empty((height, half_cols(width)), dtype=np.complex128)
+    _check(lib().ddm_b200_forward_spectrum(_p(f, C.c_double), width, height,
+                                           0 if precision == "f32" else 1, 0,
+                                           _p(out.view(np.float64), C.c_double)))
+    return out
+
+
+def azimuthal_average(values, width: int, height: int, q_max: Optional[float] = None, device: int = 0):
+    """ddm::azimuthal_average (`analysis.cpp:61-97`) -> (means [L, bins], counts [bins])."""
+    v = np.ascontiguousarray(values, dtype=np.float64)
+    L = v.shape[0]
+    cap = int(np.ceil(np.hypot(height / 2, width / 2))) + 2
+    means = np.zeros(L * cap)
+    counts = np.zeros(cap, dtype=np.int64)
+    nb = C.c_int64(0)
+    _check(lib().ddm_b200_azimuthal(_p(v, C.c_double), C.c_int64(L), width, height,
+                                    0 if q_max is None else 1,
+                                    C.c_double(0.0 if q_max is None else q_max), device,
+                                    _p(means, C.c_double), _p(counts, C.c_int64), C.c_int64(cap),
+                                    C.byref(nb)))
+    b = nb.value
+    return means[: L * b].reshape(L, b), counts[:b].copy()
+
+
+def generate(width=64, height=64, frames=256, particles=100, diffusion=0.5, psf_sigma=1.0,
+             amplitude=1000.0, background=100.0, frame_interval=1.0, seed=0) -> np.ndarray:
+    """ddm::generate (`synth.cpp:98-132`), bit-identical frames [N, H, W] uint16."""
+    out = np.empty((frames, height, width), dtype=np.uint16)
+    _check(lib().ddm_b200_generate(C.c_int64(particles), C.c_double(diffusion),
+                                   C.c_double(psf_sigma), C.c_double(amplitude),
+                                   C.c_double(background), width, height, frames,
+                                   C.c_double(frame_interval), C.c_uint64(seed),
+                                   _p(out, C.c_uint16)))
+    return out
+
+
+def run_device(frames_ptr: int, pixel_bytes: int, width: int, height: int, frames: int,
+               out_ptr: int, precision: str = "f32", out_f64: bool = False, lags=None,
+               q_max: Optional[float] = None, device: int = 0, stream: int = 0):
+    """Device-resident WITH_FT (frames and map already in HBM, e.g. torch tensors' data_ptr).
+    Returns (spatial_ms, temporal_ms, kernel_launches) of device time."""
+    lag_arr = np.ascontiguousarray(np.asarray(lags if lags is not None else [], dtype=np.int64))
+    sp, tp, nl = C.c_double(0), C.c_double(0), C.c_int(0)
+    _check(lib().ddm_b200_run_device(
+        C.c_void_p(frames_ptr), pixel_bytes, width, height, frames,
+        0 if precision == "f32" else 1, _p(lag_arr, C.c_int64) if len(lag_arr) else None,
+        C.c_int64(len(lag_arr)), 0 if q_max is None else 1,
+        C.c_double(0.0 if q_max is None else q_max), C.c_void_p(out_ptr), 1 if out_f64 else 0,
+        device, C.c_void_p(stream), C.byref(sp), C.byref(tp), C.byref(nl)))
+    return sp.value, tp.value, nl.value
