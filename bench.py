@@ -1,0 +1,314 @@
+"""Benchmark of the B200 WITH_FT structure-function path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE configs[1], the headline): 512 x 512 px x 1024 frames, d(q, m) for every
+wave vector of the half plane and every lag, f32 transforms (the reference's --precision f32
+path). Frames are the reference synthetic generator (P=100, D=0.5, seed 7).
+
+One "step" = the whole hot path over the stack: batched r2c spatial FFT + tile-major corner
+turn + fused temporal engine writing the lag-major map.
+  value : frames/s with frames resident in HBM and the map left in HBM (f32 map), device
+          time with CUDA events on the launching stream, max over ranks.
+  e2e   : the same metric through the C-ABI entry `ddm_b200_run_u16` (the reference-facing
+          `ddm::run`), pinned host frames in, f64 lag-major host map out, every step.
+  --impl reference : the reference's own ddm::run (oracle/_ref, compiled from
+          /root/reference with an FFTW-API shim) on this host's cores, same workload.
+Multi-GPU (--gpus N > 1, torchrun): each rank runs its own full stack (replicas; see
+DESIGN.md for the sharded frames + all-to-all path).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+W, H, N = 512, 512, 1024
+METRIC = "frames/s for 512×512×1024 d(q,m) at 1/2/4/8 B200; % HBM roofline"
+UNIT = "frames/s"
+WORKLOAD = "512x512 px x 1024 frames, WITH_FT d(q,m), all 131584 wave vectors x 1024 lags"
+
+
+def peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text()), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 5 + i and r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def synth_stack():
+    from paper_2012_05695_b200 import ddm
+    return ddm.generate(W, H, N, particles=100, diffusion=0.5, seed=7)
+
+
+def traffic_from_profiles():
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    try:
+        d = json.loads(p.read_text())
+        return d
+    except Exception:
+        return {}
+
+
+# --------------------------------------------------------------------------- reference arm
+
+def reference_arm(args, rank: int):
+    if rank != 0:
+        return
+    from oracle import ref
+    if not ref.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libddmref.so not built"}))
+        return
+    st = ref.generate(W, H, N, particles=100, diffusion=0.5, seed=7)
+    cores = host_cores()
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        r = ref.run(st, "with_ft", "f32", memory_bytes=1 << 40, workers=cores)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+    ms = 1e3 * float(np.mean(times))
+    value = N / (ms / 1e3)
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "width": W, "height": H, "frames": N, "precision": "f32"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                         "sample": f"full workload per step: ddm::run(MemoryFrameSource, with_ft, "
+                                   f"f32, workers={cores}) from oracle/_ref (reference core + "
+                                   f"FFTW-API shim), breakdown of last step {r.timing}"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+# --------------------------------------------------------------------------- our arm
+
+def cpu_baseline_sample():
+    """The reference CPU path on this host, bounded: one full C2 run (~10-30 s)."""
+    from oracle import ref
+    if not ref.available():
+        return None
+    st = ref.generate(W, H, N, particles=100, diffusion=0.5, seed=7)
+    cores = host_cores()
+    t0 = time.perf_counter()
+    r = ref.run(st, "with_ft", "f32", memory_bytes=1 << 40, workers=cores)
+    dt = time.perf_counter() - t0
+    return {"value": N / dt, "unit": UNIT, "cores": cores, "kind": "reference",
+            "sample": f"one full 512x512x1024 f32 run of the reference ddm::run "
+                      f"(oracle/_ref: reference core + FFTW-API shim), {dt:.2f} s wall, "
+                      f"phases {json.dumps({k: round(v, 3) for k, v in r.timing.items()})}"}
+
+
+def our_arm(args, rank: int, world: int):
+    import torch
+    from paper_2012_05695_b200 import ddm
+
+    dev = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(dev)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+
+    st = synth_stack()
+    plane = H * (W // 2 + 1)
+    frames_d = torch.from_numpy(st.view(np.uint8).reshape(-1)).to(f"cuda:{dev}")
+    out_d = torch.empty(N * plane, dtype=torch.float32, device=f"cuda:{dev}")
+    stream = torch.cuda.current_stream()
+
+    def step():
+        return ddm.run_device(frames_d.data_ptr(), 2, W, H, N, out_d.data_ptr(), "f32",
+                              out_f64=False, device=dev, stream=stream.cuda_stream)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sp_ms, tp_ms, launches = [], [], 0
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            s, t, nl = step()
+            sp_ms.append(s)
+            tp_ms.append(t)
+            launches += nl
+        e1.record(stream)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ms_total = e0.elapsed_time(e1)
+    if dist:
+        t = torch.tensor([ms_total], device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+    ms = ms_total / args.steps
+    value = world * N / (ms / 1e3)
+
+    # ---- e2e through the C-ABI with host buffers (pinned), every step H2D + D2H
+    host_frames = torch.from_numpy(st).pin_memory()
+    host_map = torch.empty(N * plane, dtype=torch.float64).pin_memory()
+    cfg = ddm.RunConfig(precision="f32", memory_bytes=1 << 40, workers=1, device=dev)
+    import ctypes as C
+    keep = []
+    c = ddm._config(cfg, keep)
+    out_lags = np.zeros(N, dtype=np.int64)
+    n_lags = C.c_int64(0)
+    counters, timing = ddm.Counters(), ddm.Timing()
+
+    def e2e_step():
+        rc = ddm.lib().ddm_b200_run_u16(C.c_void_p(host_frames.data_ptr()), W, H, N,
+                                        C.c_double(1.0), C.byref(c),
+                                        C.c_void_p(host_map.data_ptr()), C.c_int64(N * plane),
+                                        ddm._p(out_lags, C.c_int64), C.byref(n_lags),
+                                        C.byref(counters), C.byref(timing))
+        ddm._check(rc)
+
+    for _ in range(2):
+        e2e_step()
+    e2e_steps = max(3, min(args.steps, 10))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        e2e_step()
+    torch.cuda.synchronize()
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    if dist:
+        t = torch.tensor([e2e_s], device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+
+    pk, pk_kind = peaks()
+    Q = plane
+    temporal_bytes = Q * N * (8 + 4)                     # c64 spectra read + f32 map written
+    spatial_bytes = N * (2 * W * H + 8 * Q)              # u16 frames read + c64 spectra written
+    total_bytes = temporal_bytes + spatial_bytes
+    t_ms, s_ms = float(np.mean(tp_ms)), float(np.mean(sp_ms))
+    dominant = ("temporal", t_ms, temporal_bytes) if t_ms >= s_ms else ("spatial", s_ms, spatial_bytes)
+    achieved = dominant[2] / (dominant[1] / 1e3) / 1e9
+    tr = traffic_from_profiles().get(dominant[0])
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "width": W, "height": H, "frames": N, "precision": "f32",
+                   "map_dtype": "f32 (value) / f64 (e2e, reference ResultMap)",
+                   "l2": "no flush: inputs larger than L2 (0.5 GiB frames, 1.0 GiB spectra, "
+                         "0.5 GiB map per step vs 126 MB L2)",
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+        "roofline": {"bound": "hbm", "kernel": dominant[0], "achieved": achieved,
+                     "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": achieved / pk["hbm_gbs"],
+                     "peak_kind": pk_kind, "traffic": tr,
+                     "algorithmic_bytes_per_launch": dominant[2],
+                     "launch_ms": dominant[1]},
+        "stages": {"spatial_ms": s_ms, "temporal_ms": t_ms,
+                   "spatial_GBps": spatial_bytes / (s_ms / 1e3) / 1e9,
+                   "temporal_GBps": temporal_bytes / (t_ms / 1e3) / 1e9,
+                   "pipeline_GBps": total_bytes / (ms / 1e3) / 1e9,
+                   "pipeline_frac_of_hbm": total_bytes / (ms / 1e3) / 1e9 / pk["hbm_gbs"]},
+        "clocks": clk.summary(),
+        "e2e": {"value": world * N / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(st.nbytes),
+                "d2h_bytes_per_step": int(N * plane * 8), "ms_per_step": e2e_s * 1e3,
+                "path": "ddm_b200_run_u16 (C-ABI ddm::run): pinned u16 in, f64 lag-major map out"},
+        "gpu_launches": launches,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline_sample()
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true",
+                    help="skip the reference CPU sample (profiling runs)")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    if args.impl == "reference":
+        reference_arm(args, rank)
+    else:
+        our_arm(args, rank, world if "WORLD_SIZE" in os.environ else 1)
+
+
+if __name__ == "__main__":
+    main()
