@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "kernels.cuh"
@@ -39,6 +40,12 @@ void* DeviceBuffer::ensure(size_t bytes) {
 }
 
 namespace {
+
+// DDM_B200_V1=1 forces the generic shared-memory temporal kernel (A/B comparisons).
+bool use_warp_temporal(int N, int N2, int sb) {
+    static const bool v1 = std::getenv("DDM_B200_V1") != nullptr;
+    return !v1 && ddmk::temporal_warp_supported(N, N2, sb);
+}
 
 int64_t pad_len(int64_t n) {
     int64_t n2 = 1;
@@ -129,6 +136,7 @@ void build_table(std::vector<unsigned char>& out, int len, int count) {
 
 Engine::Engine(int device) : device_(device) {
     check(cudaSetDevice(device_), "cudaSetDevice");
+    check(cudaDeviceGetAttribute(&num_sms_, cudaDevAttrMultiProcessorCount, device_), "attr");
     check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
     for (auto& e : ev_) check(cudaEventCreate(&e), "cudaEventCreate");
 }
@@ -196,7 +204,8 @@ uint64_t Engine::run(const RunSpec& sp, PhaseTimes* times) {
     const int64_t N2 = pad_len(N);
     const int sb = sp.f64 ? 8 : 4;
     const size_t cs = 2 * (size_t)sb;
-    const int T = ddmk::temporal_tile(N, (int)N2, sb);
+    const bool warp_t = use_warp_temporal(N, (int)N2, sb);
+    const int T = warp_t ? 1 : ddmk::temporal_tile(N, (int)N2, sb);
     if (T == 0)
         throw std::length_error("sequence of " + std::to_string(N) +
                                 " frames exceeds the single-CTA temporal engine (max " +
@@ -251,7 +260,8 @@ uint64_t Engine::run(const RunSpec& sp, PhaseTimes* times) {
     ta.N2 = (int)N2;
     ta.tw = {(int)N2, twiddles((int)N2, sp.f64)};
     ta.tw_half = {(int)N2 / 2, twiddles((int)N2 / 2, sp.f64)};
-    ta.lag_index = static_cast<const int*>(lagidx_.get());
+    // every lag requested (the common case): kernels skip the lag lookup
+    ta.lag_index = (int64_t)sp.lags.size() == N ? nullptr : static_cast<const int*>(lagidx_.get());
     ta.out_f64 = sp.out_f64 ? 1 : 0;
     const size_t ob = sp.out_f64 ? 8 : 4;
 
@@ -310,8 +320,9 @@ uint64_t Engine::run(const RunSpec& sp, PhaseTimes* times) {
             ta.dest_of_slot = static_cast<const int64_t*>(dest_.get());
         }
         mark();
-        check(sp.f64 ? ddmk::launch_temporal<double>(ta, stream_)
-                     : ddmk::launch_temporal<float>(ta, stream_), "temporal kernel");
+        check(warp_t ? ddmk::launch_temporal_warp(ta, num_sms_, stream_)
+                     : sp.f64 ? ddmk::launch_temporal<double>(ta, stream_)
+                              : ddmk::launch_temporal<float>(ta, stream_), "temporal kernel");
         if (times) times->temporal_launches += 1;
         mark();
         if (sp.partial_mode && sp.on_partial) sp.on_partial(gi, ta.out, gc);
@@ -373,7 +384,8 @@ void Engine::sequences(const void* d_seq, int64_t q, int64_t n, bool f64, double
     const int64_t N2 = pad_len(n);
     const int sb = f64 ? 8 : 4;
     const size_t cs = 2 * (size_t)sb;
-    const int T = ddmk::temporal_tile((int)n, (int)N2, sb);
+    const bool warp_t = use_warp_temporal((int)n, (int)N2, sb);
+    const int T = warp_t ? 1 : ddmk::temporal_tile((int)n, (int)N2, sb);
     if (T == 0)
         throw std::length_error("sequence of " + std::to_string(n) +
                                 " frames exceeds the single-CTA temporal engine");
@@ -432,7 +444,8 @@ void Engine::sequences(const void* d_seq, int64_t q, int64_t n, bool f64, double
     ta.dest_of_slot = static_cast<const int64_t*>(dest_.get());
     ta.corr_out = d_corr;
     ta.mean_out = d_mean;
-    check(f64 ? ddmk::launch_temporal<double>(ta, stream_) : ddmk::launch_temporal<float>(ta, stream_),
+    check(warp_t ? ddmk::launch_temporal_warp(ta, num_sms_, stream_)
+                 : f64 ? ddmk::launch_temporal<double>(ta, stream_) : ddmk::launch_temporal<float>(ta, stream_),
           "temporal kernel");
     if (terms) {
         double* d_da = d_a_out ? d_a_out : d_out;  // never both null here when terms

@@ -113,6 +113,7 @@ private:
     const void* post_twiddles(int W, bool f64);        // exp(-2 pi i k / W), k <= W/2
 
     int device_;
+    int num_sms_ = 148;
     cudaStream_t stream_ = nullptr;
     cudaEvent_t ev_[4] = {};
     DeviceBuffer frames_, spec_, mid_, lagidx_, slotmap_, dest_, partial_, user_scratch_;

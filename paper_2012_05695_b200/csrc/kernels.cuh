@@ -61,6 +61,12 @@ cudaError_t launch_spatial(const SpatialArgs& a, cudaStream_t stream);
 template <typename S>
 cudaError_t launch_temporal(const TemporalArgs& a, cudaStream_t stream);
 
+// Warp-per-sequence temporal engine (temporal_warp.cu): f32, N2 == 2048, wave-vector-major
+// spectra (layout T = 1).
+bool temporal_warp_supported(int N, int N2, int scalar_bytes);
+size_t temporal_warp_smem();
+cudaError_t launch_temporal_warp(const TemporalArgs& a, int num_sms, cudaStream_t stream);
+
 // Shared memory / tile geometry chosen for the temporal kernel; the spectra layout T must
 // match it. Returns 0 when the sequence length is beyond what one CTA can hold.
 int temporal_tile(int N, int N2, int scalar_bytes);
