@@ -236,7 +236,10 @@ uint64_t Engine::run(const RunSpec& sp, PhaseTimes* times) {
     void* d_spec = spec_.ensure((size_t)tiles_max * N * T * cs);
     // frame chunk whose row-pass output stays in L2 (~48 MB)
     const size_t per_frame = (size_t)Wh * H * cs;
-    const int F = (int)std::max<int64_t>(1, std::min<int64_t>(N, (48u << 20) / per_frame));
+    const bool warp_s = warp_t && ddmk::spatial_warp_supported(W, H, sp.pixel_bytes, sb) &&
+                        std::getenv("DDM_B200_V1_SPATIAL") == nullptr;
+    int F = (int)std::max<int64_t>(1, std::min<int64_t>(N, (48u << 20) / per_frame));
+    if (warp_s && F > 32) F -= F % 32;  // whole frame groups per column CTA
     last_F_ = F;
     void* d_mid = mid_.ensure((size_t)F * per_frame);
 
@@ -295,8 +298,9 @@ uint64_t Engine::run(const RunSpec& sp, PhaseTimes* times) {
         for (int f0 = 0; f0 < N; f0 += F) {
             sa.frame0 = f0;
             sa.nframes = std::min(F, N - f0);
-            check(sp.f64 ? ddmk::launch_spatial<double>(sa, stream_)
-                         : ddmk::launch_spatial<float>(sa, stream_), "spatial kernels");
+            check(warp_s ? ddmk::launch_spatial_warp<float>(sa, stream_)
+                  : sp.f64 ? ddmk::launch_spatial<double>(sa, stream_)
+                           : ddmk::launch_spatial<float>(sa, stream_), "spatial kernels");
             if (times) times->spatial_launches += 2;
         }
         mark();

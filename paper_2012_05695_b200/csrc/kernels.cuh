@@ -67,6 +67,12 @@ bool temporal_warp_supported(int N, int N2, int scalar_bytes);
 size_t temporal_warp_smem();
 cudaError_t launch_temporal_warp(const TemporalArgs& a, int num_sms, cudaStream_t stream);
 
+// Register-resident spatial kernels (spatial_warp.cu): f32, power-of-two W/2 and H in
+// [16, 1024], u16/u8 frames, wave-vector-major output (layout T = 1).
+bool spatial_warp_supported(int W, int H, int pixel_bytes, int scalar_bytes);
+template <typename S>
+cudaError_t launch_spatial_warp(const SpatialArgs& a, cudaStream_t stream);
+
 // Shared memory / tile geometry chosen for the temporal kernel; the spectra layout T must
 // match it. Returns 0 when the sequence length is beyond what one CTA can hold.
 int temporal_tile(int N, int N2, int scalar_bytes);

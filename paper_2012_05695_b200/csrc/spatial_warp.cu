@@ -1,0 +1,228 @@
+// Spatial step v2 (sm_100a): register-resident group FFTs (warp_fft.cuh) for power-of-two
+// frame sizes, writing the wave-vector-major spectra the warp temporal engine streams.
+//
+// Same contract as spatial.cu (FFTW r2c 2D, `fft.cpp:34-37,86-87,128-132`, unnormalised,
+// rows=H x cols=W -> H x (W/2+1); conversion `scheduler.cpp:115-119`; corner turn
+// `scheduler.cpp:122-126`), specialised on the transform lengths:
+//   rows2  : one group of A lanes per image row. Pixel pairs (x[2k], x[2k+1]) are read as
+//            32-bit words (u16) and form the L = W/2 complex input; the even/odd split after
+//            the FFT needs Z[k] and Z[L-k], so rows pass through shared memory once and are
+//            written column-major per frame, mid[f][col][row], RB = 256/A rows per run.
+//   cols2  : one CTA = one column x F = 256/A frames; every group transforms the column of
+//            one frame; the CTA transposes through shared memory so that each retained wave
+//            vector receives F consecutive frames as one contiguous run:
+//            spec[slot * N + frame] (layout T = 1, consumed by temporal_warp.cu).
+#include <type_traits>
+
+#include "kernels.cuh"
+#include "warp_fft.cuh"
+
+namespace ddmk {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+template <int L>
+struct Split {  // L = A * B with A | B, A <= 32
+    static constexpr int log2L = L <= 1 ? 0 : 1 + Split<(L > 1 ? L / 2 : 1)>::log2L;
+};
+template <>
+struct Split<1> {
+    static constexpr int log2L = 0;
+};
+template <int L>
+__host__ __device__ constexpr int split_a() {
+    constexpr int e = Split<L>::log2L;
+    constexpr int a = 1 << (e / 2);
+    return a > 32 ? 32 : a;
+}
+
+// ---------------------------------------------------------------------------- rows
+template <typename S, typename Pix, int L>
+__global__ void __launch_bounds__(kThreads)
+rows2_kernel(const Pix* __restrict__ frames, int H, int frame0,
+             const cpx<S>* __restrict__ tw_post, cpx<S>* __restrict__ mid) {
+    constexpr int A = split_a<L>(), B = L / A;
+    constexpr int W = 2 * L, Wh = L + 1;
+    constexpr int RB = kThreads / A;                 // rows per CTA (one per group)
+    constexpr int REG = B * (A + 1) + 1;             // group region (odd stride: banks)
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cpx<S>* region_base = reinterpret_cast<cpx<S>*>(smem_raw);
+
+    const int g = threadIdx.x / A, a = threadIdx.x % A;
+    const int rblocks = (H + RB - 1) / RB;
+    const int fi = blockIdx.x / rblocks;
+    const int r0 = (blockIdx.x - fi * rblocks) * RB;
+    const int nr = min(RB, H - r0);
+    cpx<S>* reg = region_base + g * REG;
+
+    LaneTw<B, S> tw;
+    tw.init(a, L);
+
+    cpx<S> v[B];
+    if (g < nr) {
+        const Pix* row = frames + ((size_t)(frame0 + fi) * H + r0 + g) * W;
+        if constexpr (std::is_same_v<Pix, uint16_t>) {
+            const uint32_t* w32 = reinterpret_cast<const uint32_t*>(row);
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+                const uint32_t p = __ldg(w32 + a + A * b);
+                v[b] = {(S)(p & 0xFFFFu), (S)(p >> 16)};
+            }
+        } else {
+            const uint16_t* w16 = reinterpret_cast<const uint16_t*>(row);
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+                const uint16_t p = __ldg(w16 + a + A * b);
+                v[b] = {(S)(p & 0xFFu), (S)(p >> 8)};
+            }
+        }
+        group_fft<A, B, -1, S>(v, reg, a, tw);
+        // natural order into the group region: Z[k] at k
+#pragma unroll
+        for (int i = 0; i < B / A; ++i)
+#pragma unroll
+            for (int d = 0; d < A; ++d) reg[(a + i * A) + B * d] = v[i * A + d];
+    }
+    __syncthreads();
+
+    // even/odd split: X[c] = (Z[c] + conj Z[L-c]) / 2 + W_W^c (Z[c] - conj Z[L-c]) / (2i)
+    const S half = S(0.5);
+    cpx<S>* dst = mid + (size_t)fi * Wh * H + r0;
+    for (int idx = threadIdx.x; idx < nr * Wh; idx += kThreads) {
+        const int c = idx / nr, rr = idx - c * nr;
+        const cpx<S>* z = region_base + rr * REG;
+        const cpx<S> zk = z[c % L];
+        cpx<S> zc = z[(L - c) % L];
+        zc.y = -zc.y;
+        const cpx<S> e = {(zk.x + zc.x) * half, (zk.y + zc.y) * half};
+        const cpx<S> o = {(zk.y - zc.y) * half, -(zk.x - zc.x) * half};
+        dst[(size_t)c * H + rr] = cadd(e, cmul(tw_post[c], o));
+    }
+}
+
+// ---------------------------------------------------------------------------- cols
+template <typename S, int HL>
+__global__ void __launch_bounds__(kThreads)
+cols2_kernel(const cpx<S>* __restrict__ mid, int Wh, int N, int frame0, int nframes,
+             cpx<S>* __restrict__ spec, SpecLayout lay, const int* __restrict__ slot_of_flat) {
+    constexpr int A = split_a<HL>(), B = HL / A;
+    constexpr int F = kThreads / A;                  // frames per CTA (one per group)
+    constexpr int REG = B * (A + 1);
+    constexpr int SP = F + 1;                        // stage pitch (complex)
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cpx<S>* sm = reinterpret_cast<cpx<S>*>(smem_raw);
+
+    const int g = threadIdx.x / A, a = threadIdx.x % A;
+    const int fblocks = (nframes + F - 1) / F;
+    const int c = blockIdx.x / fblocks;
+    const int f0 = (blockIdx.x - c * fblocks) * F;   // within the chunk
+    const int nf = min(F, nframes - f0);
+
+    LaneTw<B, S> tw;
+    tw.init(a, HL);
+
+    cpx<S> v[B];
+    if (g < nf) {
+        const cpx<S>* col = mid + ((size_t)(f0 + g) * Wh + c) * HL;
+#pragma unroll
+        for (int b = 0; b < B; ++b) v[b] = col[a + A * b];
+        group_fft<A, B, -1, S>(v, sm + g * REG, a, tw);
+    }
+    __syncthreads();  // exchange regions are reused as the transpose stage
+    if (g < nf) {
+#pragma unroll
+        for (int i = 0; i < B / A; ++i)
+#pragma unroll
+            for (int d = 0; d < A; ++d) sm[((a + i * A) + B * d) * SP + g] = v[i * A + d];
+    }
+    __syncthreads();
+
+    const int n0 = frame0 + f0;
+    for (int idx = threadIdx.x; idx < HL * F; idx += kThreads) {
+        const int r = idx / F, f = idx - r * F;
+        if (f >= nf) continue;
+        const int64_t flat = (int64_t)r * Wh + c;
+        const int64_t k = slot_of_flat ? (int64_t)slot_of_flat[flat] : flat;
+        const int64_t s = k - lay.g_begin;
+        if (k < 0 || s < 0 || s >= lay.g_count) continue;
+        spec[s * N + n0 + f] = sm[r * SP + f];
+    }
+}
+
+template <int L>
+constexpr size_t rows_smem(size_t cs) {
+    constexpr int A = split_a<L>(), B = L / A;
+    return (size_t)(kThreads / A) * (B * (A + 1) + 1) * cs;
+}
+template <int HL>
+constexpr size_t cols_smem(size_t cs) {
+    constexpr int A = split_a<HL>(), B = HL / A;
+    const size_t ex = (size_t)(kThreads / A) * B * (A + 1);
+    const size_t st = (size_t)HL * (kThreads / A + 1);
+    return (ex > st ? ex : st) * cs;
+}
+
+template <typename S, typename Pix, int L>
+void launch_rows2(const SpatialArgs& a, cudaStream_t st) {
+    auto k = rows2_kernel<S, Pix, L>;
+    const size_t smem = rows_smem<L>(sizeof(cpx<S>));
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    constexpr int RB = kThreads / split_a<L>();
+    const int grid = a.nframes * ((a.H + RB - 1) / RB);
+    k<<<grid, kThreads, smem, st>>>(static_cast<const Pix*>(a.frames), a.H, a.frame0,
+                                    static_cast<const cpx<S>*>(a.tw_post.ptr),
+                                    static_cast<cpx<S>*>(a.mid));
+}
+
+template <typename S, int HL>
+void launch_cols2(const SpatialArgs& a, cudaStream_t st) {
+    auto k = cols2_kernel<S, HL>;
+    const size_t smem = cols_smem<HL>(sizeof(cpx<S>));
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    constexpr int F = kThreads / split_a<HL>();
+    const int Wh = a.W / 2 + 1;
+    const int grid = Wh * ((a.nframes + F - 1) / F);
+    k<<<grid, kThreads, smem, st>>>(static_cast<const cpx<S>*>(a.mid), Wh, a.N, a.frame0,
+                                    a.nframes, static_cast<cpx<S>*>(a.spec), a.layout,
+                                    a.slot_of_flat);
+}
+
+bool pow2_in(int x, int lo, int hi) { return x >= lo && x <= hi && (x & (x - 1)) == 0; }
+
+}  // namespace
+
+bool spatial_warp_supported(int W, int H, int pixel_bytes, int scalar_bytes) {
+    if (scalar_bytes != 4 || (pixel_bytes != 1 && pixel_bytes != 2)) return false;
+    return W % 2 == 0 && pow2_in(W / 2, 16, 1024) && pow2_in(H, 16, 1024);
+}
+
+template <typename S>
+cudaError_t launch_spatial_warp(const SpatialArgs& a, cudaStream_t stream) {
+    const int L = a.W / 2;
+#define DDMK_R2(LEN)                                                               \
+    case LEN:                                                                      \
+        if (a.pixel_bytes == 2) launch_rows2<S, uint16_t, LEN>(a, stream);         \
+        else launch_rows2<S, uint8_t, LEN>(a, stream);                             \
+        break;
+    switch (L) {
+        DDMK_R2(16) DDMK_R2(32) DDMK_R2(64) DDMK_R2(128) DDMK_R2(256) DDMK_R2(512) DDMK_R2(1024)
+    default: return cudaErrorInvalidValue;
+    }
+#undef DDMK_R2
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+#define DDMK_C2(LEN) \
+    case LEN: launch_cols2<S, LEN>(a, stream); break;
+    switch (a.H) {
+        DDMK_C2(16) DDMK_C2(32) DDMK_C2(64) DDMK_C2(128) DDMK_C2(256) DDMK_C2(512) DDMK_C2(1024)
+    default: return cudaErrorInvalidValue;
+    }
+#undef DDMK_C2
+    return cudaGetLastError();
+}
+
+template cudaError_t launch_spatial_warp<float>(const SpatialArgs&, cudaStream_t);
+
+}  // namespace ddmk
