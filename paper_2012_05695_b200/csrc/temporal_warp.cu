@@ -39,12 +39,14 @@ struct WarpSmem {
 };
 static_assert(sizeof(WarpSmem) % 128 == 32, "region stride must stagger banks");
 
-template <typename OutT>
+template <typename OutT, bool FULL>
 __global__ void __launch_bounds__(32 * kWarps, 1)
-temporal_warp_kernel(const cpx<float>* __restrict__ spec, int N, int64_t nq,
+temporal_warp_kernel(const cpx<float>* __restrict__ spec, int N_rt, int64_t nq,
                      const int* __restrict__ lag_index, OutT* __restrict__ out,
                      int64_t out_stride, const int64_t* __restrict__ dest_of_slot,
                      double* __restrict__ corr_out, double* __restrict__ mean_out) {
+    // FULL: N == L, every bound below folds at compile time
+    const int N = FULL ? kL : N_rt;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     WarpSmem* ws = reinterpret_cast<WarpSmem*>(smem_raw);
     cpx<float>* tb_fwd = reinterpret_cast<cpx<float>*>(ws + kWarps);  // W_N2^{32 b}, b < 32
@@ -130,23 +132,26 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, int N, int64_t nq,
             }
         }
 
-        // ---- d_a by suffix sums of q_n = p_n + p_{N-1-n}; lane a owns m = 32 a + b
+        // ---- S(m) = sum_{n >= m} (p_n + p_{N-1-n}) = (N - m) d_a(m), p = |t|^2 in f64:
+        //      p goes to D in the strided order, is read back per lane as 32 consecutive n
+        //      (plus the mirrored n), suffix-summed in lane and across lanes, and S(m) is
+        //      left in D for the epilogue; lane a owns m = 32 a + b
         {
+#pragma unroll
+            for (int b = 0; b < 32; ++b)
+                my.d[padded(lane + 32 * b)] = (double)t[b].x * t[b].x + (double)t[b].y * t[b].y;
+            __syncwarp();
             double qv[32];
             double tot = 0.0;
 #pragma unroll
             for (int b = 0; b < 32; ++b) {
                 const int n = 32 * lane + b;
                 double v = 0.0;
-                if (n < N) {
-                    cpx<float> x = st[padded(n)], y = st[padded(N - 1 - n)];
-                    x.x -= ox; x.y -= oy;
-                    y.x -= ox; y.y -= oy;
-                    v = ((double)x.x * x.x + (double)x.y * x.y) + ((double)y.x * y.x + (double)y.y * y.y);
-                }
+                if (n < N) v = my.d[padded(n)] + my.d[padded(N - 1 - n)];
                 qv[b] = v;
                 tot += v;
             }
+            __syncwarp();
             // exclusive suffix over lanes: sum of totals of lanes > lane
             double incl = tot;
 #pragma unroll
@@ -158,8 +163,7 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, int N, int64_t nq,
 #pragma unroll
             for (int b = 31; b >= 0; --b) {
                 run += qv[b];
-                const int m = 32 * lane + b;
-                if (m < N) my.d[padded(m)] = run * rcp[padded(m)];
+                my.d[padded(32 * lane + b)] = run;
             }
         }
         __syncwarp();  // stage is about to become FFT scratch
@@ -188,7 +192,8 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, int N, int64_t nq,
         __syncwarp();
 
         // ---- unfold + combine; lane a owns m = 32 a + b
-        const double inv_n2 = 1.0 / (double)kN2;
+        //      d(m) = (S(m) - 2 corr(m)) / (N - m), corr = Re R(m) / N2, d(0) = 0
+        const double two_over_n2 = 2.0 / (double)kN2;
         const float h = 0.5f;
 #pragma unroll 8
         for (int b = 0; b < 32; ++b) {
@@ -201,10 +206,9 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, int N, int64_t nq,
                 const float oy2 = -(A.x - Bc.x) * h;
                 const cpx<float> w = cmul(base_unf, tb_unf[b]);  // exp(+2 pi i m / N2)
                 const float re = ex + (w.x * ox2 - w.y * oy2);
-                const double corr = (double)re * inv_n2;
-                const double dval = my.d[padded(m)] - 2.0 * corr * rcp[padded(m)];
+                const double dval = (my.d[padded(m)] - (double)re * two_over_n2) * rcp[padded(m)];
                 my.d[padded(m)] = (m == 0) ? 0.0 : dval;
-                if (corr_out && live) corr_out[q * N + m] = corr;
+                if (corr_out && live) corr_out[q * N + m] = (double)re * (0.5 * two_over_n2);
             }
         }
         if (mean_out && live && lane == 0) {
@@ -263,14 +267,15 @@ cudaError_t launch_temporal_warp(const TemporalArgs& a, int num_sms, cudaStream_
     const int grid = (int)std::min<int64_t>(tiles, (int64_t)num_sms);
     if (grid == 0) return cudaSuccess;
     const cpx<float>* spec = static_cast<const cpx<float>*>(a.spec);
+    const bool full = a.N == kL;
     if (a.out_f64) {
-        auto k = temporal_warp_kernel<double>;
+        auto k = full ? temporal_warp_kernel<double, true> : temporal_warp_kernel<double, false>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         k<<<grid, 32 * kWarps, smem, stream>>>(spec, a.N, a.layout.g_count, a.lag_index,
                                                static_cast<double*>(a.out), a.out_stride,
                                                a.dest_of_slot, a.corr_out, a.mean_out);
     } else {
-        auto k = temporal_warp_kernel<float>;
+        auto k = full ? temporal_warp_kernel<float, true> : temporal_warp_kernel<float, false>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         k<<<grid, 32 * kWarps, smem, stream>>>(spec, a.N, a.layout.g_count, a.lag_index,
                                                static_cast<float*>(a.out), a.out_stride,
