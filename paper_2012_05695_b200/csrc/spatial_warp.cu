@@ -12,6 +12,7 @@
 //            one frame; the CTA transposes through shared memory so that each retained wave
 //            vector receives F consecutive frames as one contiguous run:
 //            spec[slot * N + frame] (layout T = 1, consumed by temporal_warp.cu).
+#include <algorithm>
 #include <type_traits>
 
 #include "kernels.cuh"
@@ -41,7 +42,7 @@ __host__ __device__ constexpr int split_a() {
 // ---------------------------------------------------------------------------- rows
 template <typename S, typename Pix, int L>
 __global__ void __launch_bounds__(kThreads)
-rows2_kernel(const Pix* __restrict__ frames, int H, int frame0,
+rows2_kernel(const Pix* __restrict__ frames, int H, int frame0, const cpx<S>* __restrict__ tw_row,
              const cpx<S>* __restrict__ tw_post, cpx<S>* __restrict__ mid) {
     constexpr int A = split_a<L>(), B = L / A;
     constexpr int W = 2 * L, Wh = L + 1;
@@ -54,11 +55,11 @@ rows2_kernel(const Pix* __restrict__ frames, int H, int frame0,
     const int rblocks = (H + RB - 1) / RB;
     const int fi = blockIdx.x / rblocks;
     const int r0 = (blockIdx.x - fi * rblocks) * RB;
-    const int nr = min(RB, H - r0);
+    constexpr int nr = RB;  // H % RB == 0 (spatial_warp_supported)
     cpx<S>* reg = region_base + g * REG;
 
     LaneTw<B, S> tw;
-    tw.init(a, L);
+    tw.init_from(tw_row, a, L);
 
     cpx<S> v[B];
     if (g < nr) {
@@ -106,7 +107,8 @@ rows2_kernel(const Pix* __restrict__ frames, int H, int frame0,
 template <typename S, int HL>
 __global__ void __launch_bounds__(kThreads)
 cols2_kernel(const cpx<S>* __restrict__ mid, int Wh, int N, int frame0, int nframes,
-             cpx<S>* __restrict__ spec, SpecLayout lay, const int* __restrict__ slot_of_flat) {
+             const cpx<S>* __restrict__ tw_col, cpx<S>* __restrict__ spec, SpecLayout lay,
+             const int* __restrict__ slot_of_flat) {
     constexpr int A = split_a<HL>(), B = HL / A;
     constexpr int F = kThreads / A;                  // frames per CTA (one per group)
     constexpr int REG = B * (A + 1);
@@ -121,7 +123,7 @@ cols2_kernel(const cpx<S>* __restrict__ mid, int Wh, int N, int frame0, int nfra
     const int nf = min(F, nframes - f0);
 
     LaneTw<B, S> tw;
-    tw.init(a, HL);
+    tw.init_from(tw_col, a, HL);
 
     cpx<S> v[B];
     if (g < nf) {
@@ -172,6 +174,7 @@ void launch_rows2(const SpatialArgs& a, cudaStream_t st) {
     constexpr int RB = kThreads / split_a<L>();
     const int grid = a.nframes * ((a.H + RB - 1) / RB);
     k<<<grid, kThreads, smem, st>>>(static_cast<const Pix*>(a.frames), a.H, a.frame0,
+                                    static_cast<const cpx<S>*>(a.tw_row.ptr),
                                     static_cast<const cpx<S>*>(a.tw_post.ptr),
                                     static_cast<cpx<S>*>(a.mid));
 }
@@ -185,7 +188,8 @@ void launch_cols2(const SpatialArgs& a, cudaStream_t st) {
     const int Wh = a.W / 2 + 1;
     const int grid = Wh * ((a.nframes + F - 1) / F);
     k<<<grid, kThreads, smem, st>>>(static_cast<const cpx<S>*>(a.mid), Wh, a.N, a.frame0,
-                                    a.nframes, static_cast<cpx<S>*>(a.spec), a.layout,
+                                    a.nframes, static_cast<const cpx<S>*>(a.tw_col.ptr),
+                                    static_cast<cpx<S>*>(a.spec), a.layout,
                                     a.slot_of_flat);
 }
 
@@ -195,7 +199,10 @@ bool pow2_in(int x, int lo, int hi) { return x >= lo && x <= hi && (x & (x - 1))
 
 bool spatial_warp_supported(int W, int H, int pixel_bytes, int scalar_bytes) {
     if (scalar_bytes != 4 || (pixel_bytes != 1 && pixel_bytes != 2)) return false;
-    return W % 2 == 0 && pow2_in(W / 2, 16, 1024) && pow2_in(H, 16, 1024);
+    if (!(W % 2 == 0 && pow2_in(W / 2, 16, 1024) && pow2_in(H, 16, 1024))) return false;
+    const int e = 31 - __builtin_clz(W / 2);
+    const int A = std::min(1 << (e / 2), 32);
+    return H % (kThreads / A) == 0;  // whole row blocks per CTA
 }
 
 template <typename S>

@@ -142,16 +142,27 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, int N_rt, int64_t nq,
                 my.d[padded(lane + 32 * b)] = (double)t[b].x * t[b].x + (double)t[b].y * t[b].y;
             __syncwarp();
             double qv[32];
-            double tot = 0.0;
 #pragma unroll
             for (int b = 0; b < 32; ++b) {
                 const int n = 32 * lane + b;
                 double v = 0.0;
                 if (n < N) v = my.d[padded(n)] + my.d[padded(N - 1 - n)];
                 qv[b] = v;
-                tot += v;
             }
             __syncwarp();
+            // in-lane suffix sums as 4 independent chains of 8, then chain offsets
+            double part[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                double r = 0.0;
+#pragma unroll
+                for (int b = 8 * c + 7; b >= 8 * c; --b) {
+                    r += qv[b];
+                    qv[b] = r;
+                }
+                part[c] = r;
+            }
+            const double tot = (part[0] + part[1]) + (part[2] + part[3]);
             // exclusive suffix over lanes: sum of totals of lanes > lane
             double incl = tot;
 #pragma unroll
@@ -159,12 +170,11 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, int N_rt, int64_t nq,
                 const double v = __shfl_down_sync(0xffffffffu, incl, o);
                 if (lane + o < 32) incl += v;
             }
-            double run = incl - tot;
+            const double base = incl - tot;
+            const double off[4] = {base + part[1] + part[2] + part[3], base + part[2] + part[3],
+                                   base + part[3], base};
 #pragma unroll
-            for (int b = 31; b >= 0; --b) {
-                run += qv[b];
-                my.d[padded(32 * lane + b)] = run;
-            }
+            for (int b = 0; b < 32; ++b) my.d[padded(32 * lane + b)] = qv[b] + off[b >> 3];
         }
         __syncwarp();  // stage is about to become FFT scratch
 

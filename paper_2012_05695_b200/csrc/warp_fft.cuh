@@ -144,6 +144,13 @@ struct LaneTw {
             hi[i] = {(S)c, (S)s};
         }
     }
+    // same values from a precomputed table tab[j] = exp(-2 pi i j / L) (global, L1-resident)
+    __device__ __forceinline__ void init_from(const cpx<S>* __restrict__ tab, int a, int L) {
+#pragma unroll
+        for (int j = 0; j < NLO; ++j) lo[j] = tab[(a * j) % L];
+#pragma unroll
+        for (int i = 0; i < NHI; ++i) hi[i] = tab[(a * 8 * i) % L];
+    }
     // forward-direction twiddle W_L^{a c}; SIGN > 0 conjugates
     template <int SIGN>
     __device__ __forceinline__ cpx<S> get(int c) const {
