@@ -29,3 +29,13 @@ for i in range(0, len(data), W):
         continue
     ops = collections.Counter(op(r) for r in blk)
     print(f"{i:5d} samp {100*s/tot:5.1f}%  exec/unit {ex/norm:9.1f}  {dict(ops.most_common(6))}")
+
+# stall reasons per block (second table)
+reasons = [h for h in hdr if h.startswith('stall_') and 'Not Issued' not in h]
+print('\nblock  ' + ' '.join(f"{r[6:12]:>7s}" for r in reasons))
+for i in range(0, len(data), W):
+    blk = data[i:i + W]
+    vals = [sum(int(r[ci[x]] or 0) for r in blk) for x in reasons]
+    if sum(vals) == 0:
+        continue
+    print(f"{i:5d}  " + ' '.join(f"{100*v/tot:7.1f}" for v in vals))
