@@ -105,13 +105,20 @@ def synth_stack():
     return ddm.generate(W, H, N, particles=100, diffusion=0.5, seed=7)
 
 
-def traffic_from_profiles():
+def traffic_from_profiles(stage: str):
+    """DRAM bytes per launch of the stage's kernel from the latest committed ncu --set full
+    capture (profiles/ncu_traffic.json, written by tools/profile_summary.py), or None."""
     p = ROOT / "profiles" / "ncu_traffic.json"
     try:
         d = json.loads(p.read_text())
-        return d
+        caps = d[d["latest"]]
+        vals = [v["dram_bytes"] for v in caps.values() if v["stage"] == stage]
+        if not vals:
+            return None
+        return {"dram_bytes_per_launch": sum(vals), "capture": d["latest"],
+                "kernels": sorted(k for k, v in caps.items() if v["stage"] == stage)}
     except Exception:
-        return {}
+        return None
 
 
 # --------------------------------------------------------------------------- reference arm
@@ -215,6 +222,14 @@ def our_arm(args, rank: int, world: int):
     value = world * N / (ms / 1e3)
 
     # ---- e2e through the C-ABI with host buffers (pinned), every step H2D + D2H
+    if args.no_e2e:
+        if rank == 0:
+            print(json.dumps({"metric": METRIC, "value": value, "ms_per_step": ms,
+                              "spatial_ms": float(np.mean(sp_ms)),
+                              "temporal_ms": float(np.mean(tp_ms)), "profiling_run": True}))
+        if dist:
+            dist.destroy_process_group()
+        return
     host_frames = torch.from_numpy(st).pin_memory()
     host_map = torch.empty(N * plane, dtype=torch.float64).pin_memory()
     cfg = ddm.RunConfig(precision="f32", memory_bytes=1 << 40, workers=1, device=dev)
@@ -260,7 +275,7 @@ def our_arm(args, rank: int, world: int):
     t_ms, s_ms = float(np.mean(tp_ms)), float(np.mean(sp_ms))
     dominant = ("temporal", t_ms, temporal_bytes) if t_ms >= s_ms else ("spatial", s_ms, spatial_bytes)
     achieved = dominant[2] / (dominant[1] / 1e3) / 1e9
-    tr = traffic_from_profiles().get(dominant[0])
+    tr = traffic_from_profiles(dominant[0])
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True,
@@ -272,7 +287,8 @@ def our_arm(args, rank: int, world: int):
                    "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
         "roofline": {"bound": "hbm", "kernel": dominant[0], "achieved": achieved,
                      "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": achieved / pk["hbm_gbs"],
-                     "peak_kind": pk_kind, "traffic": tr,
+                     "peak_kind": pk_kind,
+                     "traffic": tr["dram_bytes_per_launch"] if tr else None, "traffic_source": tr,
                      "algorithmic_bytes_per_launch": dominant[2],
                      "launch_ms": dominant[1]},
         "stages": {"spatial_ms": s_ms, "temporal_ms": t_ms,
@@ -301,6 +317,8 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true",
                     help="skip the reference CPU sample (profiling runs)")
+    ap.add_argument("--no-e2e", action="store_true",
+                    help="skip the C-ABI host-buffer leg (profiling runs)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
