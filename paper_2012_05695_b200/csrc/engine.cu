@@ -143,6 +143,9 @@ Engine::Engine(int device) : device_(device) {
 
 Engine::~Engine() {
     cudaSetDevice(device_);
+    for (auto e : timing_events_) cudaEventDestroy(e);
+    for (auto e : chunk_events_) cudaEventDestroy(e);
+    if (cols_stream_) cudaStreamDestroy(cols_stream_);
     for (auto& e : ev_)
         if (e) cudaEventDestroy(e);
     if (stream_) cudaStreamDestroy(stream_);
@@ -212,12 +215,17 @@ uint64_t Engine::run(const RunSpec& sp, PhaseTimes* times) {
                                 std::to_string(max_frames(sp.f64)) + ")");
     last_T_ = T;
 
-    // lag slots
-    std::vector<int> lag_index((size_t)N, -1);
-    for (size_t li = 0; li < sp.lags.size(); ++li) lag_index[(size_t)sp.lags[li]] = (int)li;
-    check(cudaMemcpyAsync(lagidx_.ensure((size_t)N * sizeof(int)), lag_index.data(),
-                          (size_t)N * sizeof(int), cudaMemcpyHostToDevice, stream_),
-          "lag upload");
+    // lag slots (uploaded only when the lag list changes; every-lag runs never read them)
+    const bool all_lags = (int64_t)sp.lags.size() == N;
+    if (!all_lags) {
+        std::vector<int> lag_index((size_t)N, -1);
+        for (size_t li = 0; li < sp.lags.size(); ++li) lag_index[(size_t)sp.lags[li]] = (int)li;
+        if (lag_index != lag_cache_) {
+            check(cudaMemcpy(lagidx_.ensure((size_t)N * sizeof(int)), lag_index.data(),
+                             (size_t)N * sizeof(int), cudaMemcpyHostToDevice), "lag upload");
+            lag_cache_ = std::move(lag_index);
+        }
+    }
     // flat -> retained index map (cutoff only)
     const int* d_slot = nullptr;
     std::vector<int> slot_of;
@@ -241,7 +249,12 @@ uint64_t Engine::run(const RunSpec& sp, PhaseTimes* times) {
     int F = (int)std::max<int64_t>(1, std::min<int64_t>(N, (48u << 20) / per_frame));
     if (warp_s && F > 32) F -= F % 32;  // whole frame groups per column CTA
     last_F_ = F;
-    void* d_mid = mid_.ensure((size_t)F * per_frame);
+    // register-resident path: the row pass of chunk k+1 runs beside the column pass of chunk
+    // k on a second stream, through two L2-resident `mid` buffers
+    const bool overlap = warp_s && N > F && std::getenv("DDM_SPATIAL_SERIAL") == nullptr;
+    void* d_mid = mid_.ensure((size_t)F * per_frame * (overlap ? 2 : 1));
+    if (overlap && !cols_stream_)
+        check(cudaStreamCreateWithFlags(&cols_stream_, cudaStreamNonBlocking), "cudaStreamCreate");
 
     ddmk::SpatialArgs sa;
     sa.frames = sp.d_frames;
@@ -264,19 +277,21 @@ uint64_t Engine::run(const RunSpec& sp, PhaseTimes* times) {
     ta.tw = {(int)N2, twiddles((int)N2, sp.f64)};
     ta.tw_half = {(int)N2 / 2, twiddles((int)N2 / 2, sp.f64)};
     // every lag requested (the common case): kernels skip the lag lookup
-    ta.lag_index = (int64_t)sp.lags.size() == N ? nullptr : static_cast<const int*>(lagidx_.get());
+    ta.lag_index = all_lags ? nullptr : static_cast<const int*>(lagidx_.get());
     ta.out_f64 = sp.out_f64 ? 1 : 0;
     const size_t ob = sp.out_f64 ? 8 : 4;
 
     std::vector<cudaEvent_t> evs;
-    auto mark = [&]() -> cudaEvent_t {
-        cudaEvent_t e = nullptr;
-        if (times) {
+    auto mark = [&]() {
+        if (!times) return;
+        if (evs.size() == timing_events_.size()) {
+            cudaEvent_t e = nullptr;
             check(cudaEventCreate(&e), "cudaEventCreate");
-            check(cudaEventRecord(e, stream_), "cudaEventRecord");
-            evs.push_back(e);
+            timing_events_.push_back(e);
         }
-        return e;
+        cudaEvent_t e = timing_events_[evs.size()];
+        check(cudaEventRecord(e, stream_), "cudaEventRecord");
+        evs.push_back(e);
     };
 
     uint64_t spatial_passes = 0;
@@ -295,13 +310,41 @@ uint64_t Engine::run(const RunSpec& sp, PhaseTimes* times) {
         }
         sa.layout = lay;
         mark();
-        for (int f0 = 0; f0 < N; f0 += F) {
-            sa.frame0 = f0;
-            sa.nframes = std::min(F, N - f0);
-            check(warp_s ? ddmk::launch_spatial_warp<float>(sa, stream_)
-                  : sp.f64 ? ddmk::launch_spatial<double>(sa, stream_)
-                           : ddmk::launch_spatial<float>(sa, stream_), "spatial kernels");
-            if (times) times->spatial_launches += 2;
+        if (overlap) {
+            const int chunks = (N + F - 1) / F;
+            while (chunk_events_.size() < (size_t)(2 * chunks + 1)) {
+                cudaEvent_t e = nullptr;
+                check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+                chunk_events_.push_back(e);
+            }
+            cudaEvent_t start = chunk_events_[2 * chunks];
+            check(cudaEventRecord(start, stream_), "cudaEventRecord");
+            check(cudaStreamWaitEvent(cols_stream_, start, 0), "stream wait");
+            for (int k = 0; k < chunks; ++k) {
+                cudaEvent_t rows_done = chunk_events_[2 * k], cols_done = chunk_events_[2 * k + 1];
+                sa.frame0 = k * F;
+                sa.nframes = std::min(F, N - k * F);
+                sa.mid = static_cast<char*>(d_mid) + (size_t)(k & 1) * F * per_frame;
+                // the buffer is free once the column pass of chunk k-2 has read it
+                if (k >= 2) check(cudaStreamWaitEvent(stream_, chunk_events_[2 * (k - 2) + 1], 0), "wait");
+                check(ddmk::launch_spatial_warp<float>(sa, stream_, 1), "row pass");
+                check(cudaEventRecord(rows_done, stream_), "cudaEventRecord");
+                check(cudaStreamWaitEvent(cols_stream_, rows_done, 0), "wait");
+                check(ddmk::launch_spatial_warp<float>(sa, cols_stream_, 2), "column pass");
+                check(cudaEventRecord(cols_done, cols_stream_), "cudaEventRecord");
+                if (times) times->spatial_launches += 2;
+            }
+            check(cudaStreamWaitEvent(stream_, chunk_events_[2 * (chunks - 1) + 1], 0), "join");
+            sa.mid = d_mid;
+        } else {
+            for (int f0 = 0; f0 < N; f0 += F) {
+                sa.frame0 = f0;
+                sa.nframes = std::min(F, N - f0);
+                check(warp_s ? ddmk::launch_spatial_warp<float>(sa, stream_)
+                      : sp.f64 ? ddmk::launch_spatial<double>(sa, stream_)
+                               : ddmk::launch_spatial<float>(sa, stream_), "spatial kernels");
+                if (times) times->spatial_launches += 2;
+            }
         }
         mark();
         spatial_passes += (uint64_t)N;
@@ -342,7 +385,6 @@ uint64_t Engine::run(const RunSpec& sp, PhaseTimes* times) {
             times->spatial_ms += a;
             times->temporal_ms += b;
         }
-        for (auto e : evs) cudaEventDestroy(e);
     } else {
         // lag_index / slot_of host vectors are consumed by async copies above
         check(cudaStreamSynchronize(stream_), "sync");
@@ -412,6 +454,7 @@ void Engine::sequences(const void* d_seq, int64_t q, int64_t n, bool f64, double
     for (int64_t m = 0; m < n; ++m) lag_index[(size_t)m] = (int)m;
     check(cudaMemcpyAsync(lagidx_.ensure((size_t)n * sizeof(int)), lag_index.data(),
                           (size_t)n * sizeof(int), cudaMemcpyHostToDevice, stream_), "lag upload");
+    lag_cache_.clear();  // lagidx_ no longer holds a run's lag slots
     // out[s][m]: li = m, dest(s) = s * n, out_stride = 1
     std::vector<int64_t> dest((size_t)q);
     for (int64_t s = 0; s < q; ++s) dest[(size_t)s] = s * n;

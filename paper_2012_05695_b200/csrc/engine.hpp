@@ -122,6 +122,10 @@ private:
     std::map<std::pair<int, int>, std::unique_ptr<DeviceBuffer>> post_;
     std::map<std::string, std::unique_ptr<DeviceBuffer>> named_;
     int last_T_ = 0, last_F_ = 0;
+    std::vector<int> lag_cache_;               // lag slots last uploaded to lagidx_
+    std::vector<cudaEvent_t> timing_events_;   // reusable phase-timing events
+    std::vector<cudaEvent_t> chunk_events_;    // row/column pass ordering across streams
+    cudaStream_t cols_stream_ = nullptr;       // column passes (overlapped spatial step)
     std::mutex mu_;
 };
 

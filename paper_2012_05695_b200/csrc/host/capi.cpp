@@ -201,9 +201,12 @@ int ddm_b200_run_device(const void* d_frames, int pixel_bytes, int width, int he
         std::vector<int64_t> lag_list = (lags && n_lags > 0)
                                             ? ddm::normalize_lags({lags, lags + n_lags}, frames)
                                             : ddm::all_lags(frames);
-        const auto wv = ddm::cutoff_set(width, height,
-                                        has_q_max ? std::optional<double>(q_max) : std::nullopt);
-        if (wv.count() < 1) throw ddm::InputError("wave-vector cutoff retains nothing");
+        const int64_t plane = int64_t(height) * (width / 2 + 1);
+        ddm::WaveVectorSet wv;
+        if (has_q_max) {
+            wv = ddm::cutoff_set(width, height, std::optional<double>(q_max));
+            if (wv.count() < 1) throw ddm::InputError("wave-vector cutoff retains nothing");
+        }
         ddm::detail::guard_device([&] {
             auto& eng = ddm::b200::Engine::instance(device);
             std::lock_guard<std::mutex> lock(eng.mutex());
@@ -220,16 +223,21 @@ int ddm_b200_run_device(const void* d_frames, int pixel_bytes, int width, int he
             sp.pixel_bytes = pixel_bytes;
             sp.d_frames = d_frames;
             sp.lags = lag_list;
-            sp.flat.resize(size_t(wv.count()));
+            // no cutoff: every wave vector, identity positions (no index list is built)
             sp.identity = true;
-            for (int64_t k = 0; k < wv.count(); ++k) {
-                sp.flat[size_t(k)] = wv.flat(k);
-                if (sp.flat[size_t(k)] != k) sp.identity = false;
+            int64_t count = plane;
+            if (has_q_max) {
+                count = wv.count();
+                sp.flat.resize(size_t(count));
+                for (int64_t k = 0; k < count; ++k) {
+                    sp.flat[size_t(k)] = wv.flat(k);
+                    if (sp.flat[size_t(k)] != k) sp.identity = false;
+                }
             }
-            sp.groups = {{0, wv.count()}};
+            sp.groups = {{0, count}};
             sp.d_out = d_out;
             sp.out_f64 = out_f64 != 0;
-            sp.out_stride = int64_t(height) * (width / 2 + 1);
+            sp.out_stride = plane;
             ddm::b200::PhaseTimes t;
             eng.run(sp, (spatial_ms || temporal_ms || kernel_launches) ? &t : nullptr);
             ddm::b200::check(cudaEventRecord(ev, eng.stream()), "event record");

@@ -70,8 +70,9 @@ cudaError_t launch_temporal_warp(const TemporalArgs& a, int num_sms, cudaStream_
 // Register-resident spatial kernels (spatial_warp.cu): f32, power-of-two W/2 and H in
 // [16, 1024], u16/u8 frames, wave-vector-major output (layout T = 1).
 bool spatial_warp_supported(int W, int H, int pixel_bytes, int scalar_bytes);
+// parts: 1 = row pass (frames -> mid), 2 = column pass (mid -> spectra), 3 = both
 template <typename S>
-cudaError_t launch_spatial_warp(const SpatialArgs& a, cudaStream_t stream);
+cudaError_t launch_spatial_warp(const SpatialArgs& a, cudaStream_t stream, int parts = 3);
 
 // Shared memory / tile geometry chosen for the temporal kernel; the spectra layout T must
 // match it. Returns 0 when the sequence length is beyond what one CTA can hold.

@@ -206,8 +206,9 @@ bool spatial_warp_supported(int W, int H, int pixel_bytes, int scalar_bytes) {
 }
 
 template <typename S>
-cudaError_t launch_spatial_warp(const SpatialArgs& a, cudaStream_t stream) {
+cudaError_t launch_spatial_warp(const SpatialArgs& a, cudaStream_t stream, int parts) {
     const int L = a.W / 2;
+    if (parts & 1) {
 #define DDMK_R2(LEN)                                                               \
     case LEN:                                                                      \
         if (a.pixel_bytes == 2) launch_rows2<S, uint16_t, LEN>(a, stream);         \
@@ -220,6 +221,8 @@ cudaError_t launch_spatial_warp(const SpatialArgs& a, cudaStream_t stream) {
 #undef DDMK_R2
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
+    }
+    if (!(parts & 2)) return cudaSuccess;
 #define DDMK_C2(LEN) \
     case LEN: launch_cols2<S, LEN>(a, stream); break;
     switch (a.H) {
@@ -230,6 +233,6 @@ cudaError_t launch_spatial_warp(const SpatialArgs& a, cudaStream_t stream) {
     return cudaGetLastError();
 }
 
-template cudaError_t launch_spatial_warp<float>(const SpatialArgs&, cudaStream_t);
+template cudaError_t launch_spatial_warp<float>(const SpatialArgs&, cudaStream_t, int);
 
 }  // namespace ddmk

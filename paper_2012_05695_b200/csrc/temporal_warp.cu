@@ -20,6 +20,7 @@
 // mirrored lane with shuffles; d(m) goes to the warp's D array and a CTA of 8 warps stores
 // 8 consecutive wave vectors per lag row.
 #include <algorithm>
+#include <cstdlib>
 
 #include "kernels.cuh"
 #include "warp_fft.cuh"
@@ -30,18 +31,20 @@ namespace {
 
 constexpr int kL = 1024;              // half padded length
 constexpr int kN2 = 2048;
-constexpr int kWarps = 8;             // wave vectors per tile
 constexpr int kPad = kL + kL / 32;    // slots per buffer (FFT scratch pitch 33 x 32)
 
 __device__ __forceinline__ int padded(int n) { return n + (n >> 5); }
 
+// Per-warp shared memory (16.9 KB; 12 warps + the reciprocal table fit one SM):
+//   stage   : TMA target of the sequence (dense [0, N) complex), re-read for the odd
+//             transform, then reused as f32 work space for |t|^2 and S(m)
+//   scratch : exchange buffer of the three FFTs, then the f32 lag values of the tile store
 struct WarpSmem {
-    cpx<float> stage[2][kPad];   // input double buffer (dense [0, L)), then FFT scratch
-    double d[kPad];              // S(m) at padded(m), then the output value of lag m
-    unsigned long long bar[2];   // mbarriers of the two stage buffers
-    double pad_[2];              // sizeof = 32 mod 128 B: the tile store reads 8 regions at once
+    cpx<float> stage[kPad];
+    cpx<float> scratch[kPad];
+    unsigned long long bar;
+    unsigned long long pad_;
 };
-static_assert(sizeof(WarpSmem) % 128 == 32, "region stride must stagger banks");
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -73,7 +76,43 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t phas
         : "memory");
 }
 
-template <typename OutT, bool FULL>
+// v[b] *= W_64^{b} = exp(SIGN 2 pi i b / 64): compile-time constants after unrolling
+template <int SIGN>
+__device__ __forceinline__ void premul_w64(cpx<float> (&v)[32]) {
+#pragma unroll
+    for (int b = 1; b < 32; ++b) {
+        if (b == 16) v[b] = rot90<SIGN>(v[b]);  // W_64^{16} = SIGN i
+        else v[b] = cmul(v[b], ct_w<SIGN, float>(b, 64));
+    }
+}
+
+// Length-1024 transform of the warp (lane a holds x[a + 32 b] in v[b]; on return lane c
+// holds X[c + 32 d] in v[d]).  Four-step twiddles come from a CTA table twt[c][a]
+// (conflict-free 8-byte loads): W_1024^{a c}, or for ODD W_2048^{a (2c + 1)}, where the input
+// is x[n] W_2048^{n}: its W_64^{b} part is applied before the register DFT and its lane factor
+// W_2048^{a} is folded into the table, so X = the odd outputs of the zero-padded FFT_2048.
+template <int SIGN, bool ODD>
+__device__ __forceinline__ void fft1024(cpx<float> (&v)[32], cpx<float>* scratch, int lane,
+                                        const cpx<float>* __restrict__ twt) {
+    constexpr int P = 33;
+    if constexpr (ODD) premul_w64<SIGN>(v);
+    RegDft<32, SIGN, float>::run(v);
+#pragma unroll
+    for (int c = ODD ? 0 : 1; c < 32; ++c) {
+        cpx<float> w = twt[c * 32 + lane];
+        if (SIGN > 0) w.y = -w.y;
+        v[c] = cmul(v[c], w);
+    }
+#pragma unroll
+    for (int c = 0; c < 32; ++c) scratch[c * P + lane] = v[c];
+    __syncwarp();
+#pragma unroll
+    for (int ap = 0; ap < 32; ++ap) v[ap] = scratch[lane * P + ap];
+    __syncwarp();
+    RegDft<32, SIGN, float>::run(v);
+}
+
+template <typename OutT, bool FULL, int kWarps>
 __global__ void __launch_bounds__(32 * kWarps, 1)
 temporal_warp_kernel(const cpx<float>* __restrict__ spec, int N_rt, int64_t nq,
                      const int* __restrict__ lag_index, OutT* __restrict__ out,
@@ -83,69 +122,69 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, int N_rt, int64_t nq,
     const int N = FULL ? kL : N_rt;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     WarpSmem* ws = reinterpret_cast<WarpSmem*>(smem_raw);
-    cpx<float>* tb_fwd = reinterpret_cast<cpx<float>*>(ws + kWarps);  // W_N2^{32 b}, b < 32
+    cpx<float>* tw_even = reinterpret_cast<cpx<float>*>(ws + kWarps);  // [c][a] W_1024^{a c}
+    cpx<float>* tw_odd = tw_even + 32 * 32;                              // [c][a] W_2048^{a (2c+1)}
+    float* rcp = reinterpret_cast<float*>(tw_odd + 32 * 32);             // 1 / (N - m)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     WarpSmem& my = ws[warp];
+    float* stf = reinterpret_cast<float*>(my.stage);    // f32 views
+    float* scf = reinterpret_cast<float*>(my.scratch);
 
-    if (threadIdx.x < 32) {
-        double s, c;
-        sincospi(-2.0 * (double)(32 * threadIdx.x) / kN2, &s, &c);
-        tb_fwd[threadIdx.x] = {(float)c, (float)s};
-    }
+    for (int m = threadIdx.x; m < N; m += blockDim.x) rcp[m] = (float)(1.0 / (double)(N - m));
     if (lane == 0) {
-        mbar_init(&my.bar[0]);
-        mbar_init(&my.bar[1]);
+        mbar_init(&my.bar);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    // per-lane constants: four-step twiddles W_L^{lane c}, W_N2^{lane}, W_N2^{-lane}
-    LaneTw<32, float> tw;
-    tw.init(lane, kL);
-    cpx<float> base_fwd, base_unf;
+    for (int i = threadIdx.x; i < 32 * 32; i += blockDim.x) {
+        const int c = i >> 5, a = i & 31;
+        double sn, cs;
+        sincospi(-2.0 * (double)(a * c) / kL, &sn, &cs);
+        tw_even[i] = {(float)cs, (float)sn};
+        sincospi(-2.0 * (double)(a * (2 * c + 1)) / kN2, &sn, &cs);
+        tw_odd[i] = {(float)cs, (float)sn};
+    }
+    cpx<float> base_unf;  // W_N2^{-lane}
     {
-        double s, c;
-        sincospi(-2.0 * (double)lane / kN2, &s, &c);
-        base_fwd = {(float)c, (float)s};
-        base_unf = {(float)c, (float)-s};
+        double sn, cs;
+        sincospi(2.0 * (double)lane / kN2, &sn, &cs);
+        base_unf = {(float)cs, (float)sn};
     }
     const float inv_nf = 1.0f / (float)N;
     __syncthreads();
 
     const int64_t ntiles = (nq + kWarps - 1) / kWarps;
     const uint32_t bytes = (uint32_t)N * 8u;
-    auto prefetch = [&](int64_t tile, int buf) {
+    auto prefetch = [&](int64_t tile) {
         const int64_t q = tile * kWarps + warp;
         if (lane == 0 && tile < ntiles && q < nq)
-            bulk_load(my.stage[buf], spec + q * (int64_t)N, bytes, &my.bar[buf]);
+            bulk_load(my.stage, spec + q * (int64_t)N, bytes, &my.bar);
     };
 
-    int buf = 0;
-    uint32_t phase[2] = {0u, 0u};
-    prefetch(blockIdx.x, 0);
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, buf ^= 1) {
-        prefetch(tile + gridDim.x, buf ^ 1);
+    uint32_t phase = 0u;
+    prefetch(blockIdx.x);
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int64_t q = tile * kWarps + warp;
         const bool live = q < nq;
-        cpx<float>* st = my.stage[buf];
         if (live) {
-            mbar_wait(&my.bar[buf], phase[buf]);
-            phase[buf] ^= 1u;
+            mbar_wait(&my.bar, phase);
+            phase ^= 1u;
         }
 
         // ---- load (lane a holds s[a + 32 b]), mean by a pairwise f32 sum, shift
-        cpx<float> t[32];
+        cpx<float> v[32];
 #pragma unroll
         for (int b = 0; b < 32; ++b) {
             const int n = lane + 32 * b;
-            t[b] = (live && n < N) ? st[n] : cpx<float>{0.f, 0.f};
+            v[b] = (live && n < N) ? my.stage[n] : cpx<float>{0.f, 0.f};
         }
         float mx, my_;
         {
             float ax[16], ay[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
-                ax[i] = t[i].x + t[i + 16].x;
-                ay[i] = t[i].y + t[i + 16].y;
+                ax[i] = v[i].x + v[i + 16].x;
+                ay[i] = v[i].y + v[i + 16].y;
             }
 #pragma unroll
             for (int w = 8; w > 0; w >>= 1)
@@ -167,91 +206,95 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, int N_rt, int64_t nq,
 #pragma unroll
         for (int b = 0; b < 32; ++b) {
             if (lane + 32 * b < N) {
-                t[b].x -= mx;
-                t[b].y -= my_;
+                v[b].x -= mx;
+                v[b].y -= my_;
             }
         }
 
-        // ---- S(m) = sum_{n >= m} (p_n + p_{N-1-n}) = (N - m) d_a(m), p = |t|^2 in f64:
-        //      p goes to D in the strided order, is read back per lane as 32 consecutive n
-        //      (plus the mirrored n), suffix-summed in lane and across lanes; S(m) stays in D
+        // ---- even outputs of the zero-padded FFT_2048: FFT_1024(t); P in f32 (`temporal.cpp:60-64`),
+        //      kept in registers while the odd half is transformed
+        float pe[32];
+        fft1024<-1, false>(v, my.scratch, lane, tw_even);
+#pragma unroll
+        for (int d = 0; d < 32; ++d) pe[d] = v[d].x * v[d].x + v[d].y * v[d].y;
+
+        // ---- odd outputs: reload t, keep |t|^2 (f32) in the stage for the averages term
+#pragma unroll
+        for (int b = 0; b < 32; ++b) {
+            const int n = lane + 32 * b;
+            cpx<float> x = (live && n < N) ? my.stage[n] : cpx<float>{0.f, 0.f};
+            if (n < N) {
+                x.x -= mx;
+                x.y -= my_;
+            }
+            v[b] = x;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int b = 0; b < 32; ++b)
+            stf[padded(lane + 32 * b)] = v[b].x * v[b].x + v[b].y * v[b].y;
+        fft1024<-1, true>(v, my.scratch, lane, tw_odd);
+#pragma unroll
+        for (int d = 0; d < 32; ++d) v[d] = {pe[d], v[d].x * v[d].x + v[d].y * v[d].y};
+
+        // ---- half-length inverse: lane c holds U[c + 32 d] in v[d]
+        fft1024<+1, false>(v, my.scratch, lane, tw_even);
+
+        // ---- S(m) = sum_{n >= m} (p_n + p_{N-1-n}) = (N - m) d_a(m)  (`temporal.cpp:19-42`):
+        //      lane a scans n = 32 a + j in f32, lane totals are suffix-summed in f64
+        float sv[32];
         {
+            float qv[32];
 #pragma unroll
-            for (int b = 0; b < 32; ++b)
-                my.d[padded(lane + 32 * b)] = (double)t[b].x * t[b].x + (double)t[b].y * t[b].y;
-            __syncwarp();
-            double qv[32];
-#pragma unroll
-            for (int b = 0; b < 32; ++b) {
-                const int n = 32 * lane + b;
-                qv[b] = (n < N) ? my.d[padded(n)] + my.d[padded(N - 1 - n)] : 0.0;
+            for (int j = 0; j < 32; ++j) {
+                const int n = 32 * lane + j;
+                qv[j] = (n < N) ? stf[padded(n)] + stf[padded(N - 1 - n)] : 0.f;
             }
-            __syncwarp();
-            double part[4];
+            float r = 0.f;
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                double r = 0.0;
-#pragma unroll
-                for (int b = 8 * c + 7; b >= 8 * c; --b) {
-                    r += qv[b];
-                    qv[b] = r;
-                }
-                part[c] = r;
+            for (int j = 31; j >= 0; --j) {
+                r += qv[j];
+                qv[j] = r;
             }
-            const double tot = (part[0] + part[1]) + (part[2] + part[3]);
-            double incl = tot;
+            double incl = (double)r;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
-                const double v = __shfl_down_sync(0xffffffffu, incl, o);
-                if (lane + o < 32) incl += v;
+                const double t = __shfl_down_sync(0xffffffffu, incl, o);
+                if (lane + o < 32) incl += t;
             }
-            const double base = incl - tot;
-            const double off[4] = {base + part[1] + part[2] + part[3], base + part[2] + part[3],
-                                   base + part[3], base};
+            const float base = (float)(incl - (double)r);
+            __syncwarp();
+            float* sarea = stf + kPad;  // second half of the stage
 #pragma unroll
-            for (int b = 0; b < 32; ++b) my.d[padded(32 * lane + b)] = qv[b] + off[b >> 3];
+            for (int j = 0; j < 32; ++j) sarea[padded(32 * lane + j)] = qv[j] + base;
+            __syncwarp();
+#pragma unroll
+            for (int d = 0; d < 32; ++d) sv[d] = sarea[padded(lane + 32 * d)];
+            __syncwarp();
         }
-
-        // ---- forward: even outputs FFT_L(t), odd outputs FFT_L(t * W_N2^n)
-        float pe[32];
-        {
-            cpx<float> u[32];
-#pragma unroll
-            for (int b = 0; b < 32; ++b) u[b] = t[b];
-            group_fft<32, 32, -1, float>(u, st, lane, tw);
-#pragma unroll
-            for (int d = 0; d < 32; ++d) pe[d] = u[d].x * u[d].x + u[d].y * u[d].y;
-        }
-        cpx<float> z[32];
-#pragma unroll
-        for (int b = 0; b < 32; ++b) z[b] = cmul(t[b], cmul(base_fwd, tb_fwd[b]));
-        group_fft<32, 32, -1, float>(z, st, lane, tw);
-#pragma unroll
-        for (int d = 0; d < 32; ++d) z[d] = {pe[d], z[d].x * z[d].x + z[d].y * z[d].y};
-
-        // ---- half-length inverse: lane c holds U[c + 32 d] in z[d]
-        group_fft<32, 32, +1, float>(z, st, lane, tw);
+        // the stage is free: start the next sequence's copy
+        prefetch(tile + gridDim.x);
 
         // ---- unfold + combine on the lane's own m = c + 32 d; U[L - m] sits in lane
         //      (32 - c) mod 32, register 31 - d (lane 0: its own register (32 - d) mod 32)
         //      2 Re R(m) = (A.x + B.x) + w.x (A.y + B.y) + w.y (A.x - B.x), w = W_N2^{-m}
+        //      d(m) = (S(m) - 2 corr(m)) / (N - m), 2 corr(m) = 2 Re R(m) / N2
         const int src = (32 - lane) & 31;
-        const double inv_n2 = 1.0 / (double)kN2;
+        constexpr float inv_n2 = 1.0f / (float)kN2;
 #pragma unroll
         for (int d = 0; d < 32; ++d) {
             const int m = lane + 32 * d;
             cpx<float> Bc;
-            Bc.x = __shfl_sync(0xffffffffu, z[31 - d].x, src);
-            Bc.y = __shfl_sync(0xffffffffu, z[31 - d].y, src);
-            if (lane == 0) Bc = z[(32 - d) & 31];
-            const cpx<float> A = z[d];
+            Bc.x = __shfl_sync(0xffffffffu, v[31 - d].x, src);
+            Bc.y = __shfl_sync(0xffffffffu, v[31 - d].y, src);
+            if (lane == 0) Bc = v[(32 - d) & 31];
+            const cpx<float> A = v[d];
             const cpx<float> w = cmul(base_unf, ct_w<+1, float>(32 * d, kN2));  // exp(+2 pi i m / N2)
             const float re2 = (A.x + Bc.x) + (w.x * (A.y + Bc.y) + w.y * (A.x - Bc.x));
             if (m < N) {
-                const double corr2 = (double)re2 * inv_n2;  // 2 corr(m)
-                const double val = (my.d[padded(m)] - corr2) * __drcp_rn((double)(N - m));
-                my.d[padded(m)] = (m == 0) ? 0.0 : val;
-                if (corr_out && live) corr_out[q * N + m] = 0.5 * corr2;
+                const float val = fmaf(-re2, inv_n2, sv[d]) * rcp[m];
+                scf[padded(m)] = (m == 0) ? 0.f : val;
+                if (corr_out && live) corr_out[q * N + m] = 0.5 * (double)re2 / (double)kN2;
             }
         }
         if (mean_out && live && lane == 0) {
@@ -259,34 +302,37 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, int N_rt, int64_t nq,
             mean_out[2 * q + 1] = (double)my_;
         }
 
-        // ---- tile store: lag rows of 8 consecutive wave vectors
+        // ---- tile store: lag rows of 12 consecutive wave vectors (48 B runs)
         __syncthreads();
         const int64_t q0 = tile * kWarps;
         if (!lag_index && !dest_of_slot && q0 + kWarps <= nq) {
-            // every lag, identity destinations: one thread per lag row, 8 values per store
             for (int m = threadIdx.x; m < N; m += blockDim.x) {
-                OutT v[kWarps];
+                OutT vv[kWarps];
 #pragma unroll
-                for (int j = 0; j < kWarps; ++j) v[j] = (OutT)ws[j].d[padded(m)];
+                for (int j = 0; j < kWarps; ++j)
+                    vv[j] = (OutT) reinterpret_cast<const float*>(ws[j].scratch)[padded(m)];
                 OutT* dst = out + (int64_t)m * out_stride + q0;
                 if constexpr (sizeof(OutT) == 4) {
                     if (((uintptr_t)dst & 15) == 0) {
-                        reinterpret_cast<float4*>(dst)[0] = make_float4(v[0], v[1], v[2], v[3]);
-                        reinterpret_cast<float4*>(dst)[1] = make_float4(v[4], v[5], v[6], v[7]);
+#pragma unroll
+                        for (int k = 0; k < kWarps / 4; ++k)
+                            reinterpret_cast<float4*>(dst)[k] =
+                                make_float4(vv[4 * k], vv[4 * k + 1], vv[4 * k + 2], vv[4 * k + 3]);
                         continue;
                     }
                 }
 #pragma unroll
-                for (int j = 0; j < kWarps; ++j) dst[j] = v[j];
+                for (int j = 0; j < kWarps; ++j) dst[j] = vv[j];
             }
         } else {
             for (int idx = threadIdx.x; idx < N * kWarps; idx += blockDim.x) {
-                const int m = idx >> 3, j = idx & 7;
+                const int m = idx / kWarps, j = idx - m * kWarps;
                 if (q0 + j >= nq) continue;
                 const int li = lag_index ? lag_index[m] : m;
                 if (li < 0) continue;
                 const int64_t dst = dest_of_slot ? dest_of_slot[q0 + j] : q0 + j;
-                out[(int64_t)li * out_stride + dst] = (OutT)ws[j].d[padded(m)];
+                out[(int64_t)li * out_stride + dst] =
+                    (OutT) reinterpret_cast<const float*>(ws[j].scratch)[padded(m)];
             }
         }
         __syncthreads();
@@ -300,30 +346,44 @@ bool temporal_warp_supported(int N, int N2, int scalar_bytes) {
     return scalar_bytes == 4 && N2 == kN2 && N > kL / 2 && N <= kL && N % 2 == 0;
 }
 
-size_t temporal_warp_smem() { return sizeof(WarpSmem) * kWarps + 32 * sizeof(cpx<float>); }
+namespace {
 
-cudaError_t launch_temporal_warp(const TemporalArgs& a, int num_sms, cudaStream_t stream) {
-    const size_t smem = temporal_warp_smem();
-    const int64_t tiles = (a.layout.g_count + kWarps - 1) / kWarps;
+// warps (wave vectors) per CTA: 8 (255 registers, no spills); DDM_TW_WARPS=12 selects the
+// 12-warp build (168 registers) for A/B runs
+int tw_warps() {
+    static const int w = [] {
+        const char* e = std::getenv("DDM_TW_WARPS");
+        return (e && std::atoi(e) == 12) ? 12 : 8;
+    }();
+    return w;
+}
+
+template <int W, typename OutT>
+cudaError_t launch_w(const TemporalArgs& a, int num_sms, cudaStream_t stream) {
+    const size_t smem = sizeof(WarpSmem) * W + 2 * 32 * 32 * sizeof(cpx<float>) + kL * sizeof(float);
+    const int64_t tiles = (a.layout.g_count + W - 1) / W;
     const int grid = (int)std::min<int64_t>(tiles, (int64_t)num_sms);
     if (grid == 0) return cudaSuccess;
-    if (reinterpret_cast<uintptr_t>(a.spec) % 16 != 0) return cudaErrorMisalignedAddress;
     const cpx<float>* spec = static_cast<const cpx<float>*>(a.spec);
-    const bool full = a.N == kL;
-    if (a.out_f64) {
-        auto k = full ? temporal_warp_kernel<double, true> : temporal_warp_kernel<double, false>;
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k<<<grid, 32 * kWarps, smem, stream>>>(spec, a.N, a.layout.g_count, a.lag_index,
-                                               static_cast<double*>(a.out), a.out_stride,
-                                               a.dest_of_slot, a.corr_out, a.mean_out);
-    } else {
-        auto k = full ? temporal_warp_kernel<float, true> : temporal_warp_kernel<float, false>;
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k<<<grid, 32 * kWarps, smem, stream>>>(spec, a.N, a.layout.g_count, a.lag_index,
-                                               static_cast<float*>(a.out), a.out_stride,
-                                               a.dest_of_slot, a.corr_out, a.mean_out);
-    }
+    auto k = a.N == kL ? temporal_warp_kernel<OutT, true, W> : temporal_warp_kernel<OutT, false, W>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k<<<grid, 32 * W, smem, stream>>>(spec, a.N, a.layout.g_count, a.lag_index,
+                                      static_cast<OutT*>(a.out), a.out_stride, a.dest_of_slot,
+                                      a.corr_out, a.mean_out);
     return cudaGetLastError();
+}
+
+}  // namespace
+
+size_t temporal_warp_smem() {
+    return sizeof(WarpSmem) * tw_warps() + 2 * 32 * 32 * sizeof(cpx<float>) + kL * sizeof(float);
+}
+
+cudaError_t launch_temporal_warp(const TemporalArgs& a, int num_sms, cudaStream_t stream) {
+    if (reinterpret_cast<uintptr_t>(a.spec) % 16 != 0) return cudaErrorMisalignedAddress;
+    if (tw_warps() == 8)
+        return a.out_f64 ? launch_w<8, double>(a, num_sms, stream) : launch_w<8, float>(a, num_sms, stream);
+    return a.out_f64 ? launch_w<12, double>(a, num_sms, stream) : launch_w<12, float>(a, num_sms, stream);
 }
 
 }  // namespace ddmk
