@@ -47,6 +47,22 @@ struct GroupPlan {
 
 GroupPlan plan_with_ft(std::int64_t q_count, std::int64_t frames, const MemoryBudget& budget);
 
+/// Sharded WITH_FT over `ranks` GPUs (b200 extension). Rank r transforms
+/// frames [frame_begin[r], frame_begin[r+1]) in the spatial step and owns wave vectors
+/// [q_begin[r], q_begin[r+1]) in the temporal step; the wave-vector slices are the
+/// reference's GroupPlan with capacity ceil(Q / ranks) (plan_with_ft), so every rank's output
+/// is one PartialResult. Frame shards are even-sized where N allows (bulk-copy alignment).
+struct ShardPlan {
+    int ranks = 1;
+    std::int64_t frames = 0, q_count = 0;
+    std::vector<std::int64_t> frame_begin;  // ranks + 1
+    std::vector<std::int64_t> q_begin;      // ranks + 1
+    std::int64_t frames_of(int r) const { return frame_begin[r + 1] - frame_begin[r]; }
+    std::int64_t q_of(int r) const { return q_begin[r + 1] - q_begin[r]; }
+};
+
+ShardPlan plan_shards(std::int64_t q_count, std::int64_t frames, int ranks);
+
 struct RunConfig {
     Algorithm algorithm = Algorithm::WithFt;
     Precision precision = Precision::F64;

@@ -107,6 +107,34 @@ int ddm_b200_run_device(const void* d_frames, int pixel_bytes, int width, int he
                         void* stream, double* spatial_ms, double* temporal_ms,
                         int* kernel_launches);
 
+/* ---- Sharded WITH_FT over several GPUs (one process per GPU).  The reference
+   runs one process; its out-of-core GroupPlan (scheduler.cpp:365-384) is what the shards
+   follow, so rank r's temporal output is the PartialResult of group r (archive.hpp:48-61).
+   Step 1 (spatial_shard) -> corner-turn all-to-all (NCCL, caller) -> step 2
+   (temporal_segments). */
+
+/* ddm::plan_shards: frame_begin / q_begin receive ranks + 1 offsets each. */
+int ddm_b200_shard_plan(int64_t q_count, int64_t frames, int ranks, int64_t* frame_begin,
+                        int64_t* q_begin);
+
+/* Step 1 on one rank, replacing run_with_ft's frame loop (scheduler.cpp:108-127) for the
+   rank's frames: d_frames [frames][height][width] (u16 / u8) -> d_spec, every wave vector of
+   the half plane, q-major [height*(width/2+1)][frames] complex (f32 or f64 pairs).  The rows
+   [q_begin[d], q_begin[d+1]) are the block sent to rank d. Ordered after `stream`. */
+int ddm_b200_spatial_shard_device(const void* d_frames, int pixel_bytes, int width, int height,
+                                  int frames, int precision, void* d_spec, int device,
+                                  void* stream, double* ms);
+
+/* Step 2 on one rank, replacing the per-sequence loop (scheduler.cpp:146-162) for its group:
+   d_recv is the all-to-all receive buffer, [source s][q_count][seg_frames[s]] complex;
+   sequence q is the concatenation of its source segments.  Writes the lag-major map
+   d_out[li * out_stride + q] (f32 or f64) for the requested lags (NULL/0 = all). */
+int ddm_b200_temporal_segments_device(const void* d_recv, int64_t q_count, int n_segments,
+                                      const int64_t* seg_frames, int precision,
+                                      const int64_t* lags, int64_t n_lags, void* d_out,
+                                      int64_t out_stride, int out_f64, int device, void* stream,
+                                      double* ms);
+
 /* Batched SequenceEngine<S>::with_ft (proj/core/src/temporal.cpp:77-112): q sequences of n
    complex values, interleaved (re, im) f64, q-major; the working precision is `precision`
    (values are rounded to f32 first when precision = 0, as a complex<float> caller would).

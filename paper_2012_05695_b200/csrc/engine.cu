@@ -199,6 +199,85 @@ int64_t max_frames(bool f64) {
     return best;
 }
 
+ddmk::SpatialArgs Engine::spatial_args(const void* d_frames, int pixel_bytes, int W, int H, int N,
+                                       bool f64) {
+    ddmk::SpatialArgs sa;
+    sa.frames = d_frames;
+    sa.pixel_bytes = pixel_bytes;
+    sa.W = W;
+    sa.H = H;
+    sa.N = N;
+    const int Lr = (W % 2 == 0) ? W / 2 : W;
+    sa.tw_row = {Lr, twiddles(Lr, f64)};
+    sa.tw_post = {W, post_twiddles(W, f64)};
+    sa.tw_col = {H, twiddles(H, f64)};
+    return sa;
+}
+
+void Engine::spatial_pass(ddmk::SpatialArgs sa, bool f64, bool warp_s, PhaseTimes* times) {
+    const int N = sa.N;
+    const size_t per_frame = (size_t)(sa.W / 2 + 1) * sa.H * (f64 ? 16 : 8);
+    // frame chunk whose row-pass output stays in L2 (~48 MB)
+    int F = (int)std::max<int64_t>(1, std::min<int64_t>(N, (48u << 20) / per_frame));
+    if (warp_s && F > 32) F -= F % 32;  // whole frame groups per column CTA
+    last_F_ = F;
+    // register-resident path: the row pass of chunk k+1 runs beside the column pass of chunk
+    // k on a second stream, through two L2-resident `mid` buffers
+    const bool overlap = warp_s && N > F && std::getenv("DDM_SPATIAL_SERIAL") == nullptr;
+    void* d_mid = mid_.ensure((size_t)F * per_frame * (overlap ? 2 : 1));
+    sa.mid = d_mid;
+    if (overlap) {
+        if (!cols_stream_)
+            check(cudaStreamCreateWithFlags(&cols_stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+        const int chunks = (N + F - 1) / F;
+        while (chunk_events_.size() < (size_t)(2 * chunks + 1)) {
+            cudaEvent_t e = nullptr;
+            check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+            chunk_events_.push_back(e);
+        }
+        cudaEvent_t start = chunk_events_[2 * chunks];
+        check(cudaEventRecord(start, stream_), "cudaEventRecord");
+        check(cudaStreamWaitEvent(cols_stream_, start, 0), "stream wait");
+        for (int k = 0; k < chunks; ++k) {
+            cudaEvent_t rows_done = chunk_events_[2 * k], cols_done = chunk_events_[2 * k + 1];
+            sa.frame0 = k * F;
+            sa.nframes = std::min(F, N - k * F);
+            sa.mid = static_cast<char*>(d_mid) + (size_t)(k & 1) * F * per_frame;
+            // the buffer is free once the column pass of chunk k-2 has read it
+            if (k >= 2) check(cudaStreamWaitEvent(stream_, chunk_events_[2 * (k - 2) + 1], 0), "wait");
+            check(ddmk::launch_spatial_warp<float>(sa, stream_, 1), "row pass");
+            check(cudaEventRecord(rows_done, stream_), "cudaEventRecord");
+            check(cudaStreamWaitEvent(cols_stream_, rows_done, 0), "wait");
+            check(ddmk::launch_spatial_warp<float>(sa, cols_stream_, 2), "column pass");
+            check(cudaEventRecord(cols_done, cols_stream_), "cudaEventRecord");
+            if (times) times->spatial_launches += 2;
+        }
+        check(cudaStreamWaitEvent(stream_, chunk_events_[2 * (chunks - 1) + 1], 0), "join");
+    } else {
+        for (int f0 = 0; f0 < N; f0 += F) {
+            sa.frame0 = f0;
+            sa.nframes = std::min(F, N - f0);
+            check(warp_s ? ddmk::launch_spatial_warp<float>(sa, stream_)
+                  : f64 ? ddmk::launch_spatial<double>(sa, stream_)
+                        : ddmk::launch_spatial<float>(sa, stream_), "spatial kernels");
+            if (times) times->spatial_launches += 2;
+        }
+    }
+}
+
+const int* Engine::upload_lags(const std::vector<int64_t>& lags, int N) {
+    // every lag requested (the common case): kernels skip the lag lookup
+    if ((int64_t)lags.size() == N) return nullptr;
+    std::vector<int> lag_index((size_t)N, -1);
+    for (size_t li = 0; li < lags.size(); ++li) lag_index[(size_t)lags[li]] = (int)li;
+    if (lag_index != lag_cache_) {
+        check(cudaMemcpy(lagidx_.ensure((size_t)N * sizeof(int)), lag_index.data(),
+                         (size_t)N * sizeof(int), cudaMemcpyHostToDevice), "lag upload");
+        lag_cache_ = std::move(lag_index);
+    }
+    return static_cast<const int*>(lagidx_.get());
+}
+
 uint64_t Engine::run(const RunSpec& sp, PhaseTimes* times) {
     check(cudaSetDevice(device_), "cudaSetDevice");
     const int W = sp.W, H = sp.H, N = sp.N;
@@ -216,16 +295,7 @@ uint64_t Engine::run(const RunSpec& sp, PhaseTimes* times) {
     last_T_ = T;
 
     // lag slots (uploaded only when the lag list changes; every-lag runs never read them)
-    const bool all_lags = (int64_t)sp.lags.size() == N;
-    if (!all_lags) {
-        std::vector<int> lag_index((size_t)N, -1);
-        for (size_t li = 0; li < sp.lags.size(); ++li) lag_index[(size_t)sp.lags[li]] = (int)li;
-        if (lag_index != lag_cache_) {
-            check(cudaMemcpy(lagidx_.ensure((size_t)N * sizeof(int)), lag_index.data(),
-                             (size_t)N * sizeof(int), cudaMemcpyHostToDevice), "lag upload");
-            lag_cache_ = std::move(lag_index);
-        }
-    }
+    const int* d_lag_index = upload_lags(sp.lags, N);
     // flat -> retained index map (cutoff only)
     const int* d_slot = nullptr;
     std::vector<int> slot_of;
@@ -242,33 +312,11 @@ uint64_t Engine::run(const RunSpec& sp, PhaseTimes* times) {
     for (auto& g : sp.groups) gmax = std::max(gmax, g.second - g.first);
     const int64_t tiles_max = (gmax + T - 1) / T;
     void* d_spec = spec_.ensure((size_t)tiles_max * N * T * cs);
-    // frame chunk whose row-pass output stays in L2 (~48 MB)
-    const size_t per_frame = (size_t)Wh * H * cs;
     const bool warp_s = warp_t && ddmk::spatial_warp_supported(W, H, sp.pixel_bytes, sb) &&
                         std::getenv("DDM_B200_V1_SPATIAL") == nullptr;
-    int F = (int)std::max<int64_t>(1, std::min<int64_t>(N, (48u << 20) / per_frame));
-    if (warp_s && F > 32) F -= F % 32;  // whole frame groups per column CTA
-    last_F_ = F;
-    // register-resident path: the row pass of chunk k+1 runs beside the column pass of chunk
-    // k on a second stream, through two L2-resident `mid` buffers
-    const bool overlap = warp_s && N > F && std::getenv("DDM_SPATIAL_SERIAL") == nullptr;
-    void* d_mid = mid_.ensure((size_t)F * per_frame * (overlap ? 2 : 1));
-    if (overlap && !cols_stream_)
-        check(cudaStreamCreateWithFlags(&cols_stream_, cudaStreamNonBlocking), "cudaStreamCreate");
-
-    ddmk::SpatialArgs sa;
-    sa.frames = sp.d_frames;
-    sa.pixel_bytes = sp.pixel_bytes;
-    sa.W = W;
-    sa.H = H;
-    sa.N = N;
-    sa.mid = d_mid;
+    ddmk::SpatialArgs sa = spatial_args(sp.d_frames, sp.pixel_bytes, W, H, N, sp.f64);
     sa.spec = d_spec;
     sa.slot_of_flat = d_slot;
-    const int Lr = (W % 2 == 0) ? W / 2 : W;
-    sa.tw_row = {Lr, twiddles(Lr, sp.f64)};
-    sa.tw_post = {W, post_twiddles(W, sp.f64)};
-    sa.tw_col = {H, twiddles(H, sp.f64)};
 
     ddmk::TemporalArgs ta;
     ta.spec = d_spec;
@@ -277,7 +325,7 @@ uint64_t Engine::run(const RunSpec& sp, PhaseTimes* times) {
     ta.tw = {(int)N2, twiddles((int)N2, sp.f64)};
     ta.tw_half = {(int)N2 / 2, twiddles((int)N2 / 2, sp.f64)};
     // every lag requested (the common case): kernels skip the lag lookup
-    ta.lag_index = all_lags ? nullptr : static_cast<const int*>(lagidx_.get());
+    ta.lag_index = d_lag_index;
     ta.out_f64 = sp.out_f64 ? 1 : 0;
     const size_t ob = sp.out_f64 ? 8 : 4;
 
@@ -310,42 +358,7 @@ uint64_t Engine::run(const RunSpec& sp, PhaseTimes* times) {
         }
         sa.layout = lay;
         mark();
-        if (overlap) {
-            const int chunks = (N + F - 1) / F;
-            while (chunk_events_.size() < (size_t)(2 * chunks + 1)) {
-                cudaEvent_t e = nullptr;
-                check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
-                chunk_events_.push_back(e);
-            }
-            cudaEvent_t start = chunk_events_[2 * chunks];
-            check(cudaEventRecord(start, stream_), "cudaEventRecord");
-            check(cudaStreamWaitEvent(cols_stream_, start, 0), "stream wait");
-            for (int k = 0; k < chunks; ++k) {
-                cudaEvent_t rows_done = chunk_events_[2 * k], cols_done = chunk_events_[2 * k + 1];
-                sa.frame0 = k * F;
-                sa.nframes = std::min(F, N - k * F);
-                sa.mid = static_cast<char*>(d_mid) + (size_t)(k & 1) * F * per_frame;
-                // the buffer is free once the column pass of chunk k-2 has read it
-                if (k >= 2) check(cudaStreamWaitEvent(stream_, chunk_events_[2 * (k - 2) + 1], 0), "wait");
-                check(ddmk::launch_spatial_warp<float>(sa, stream_, 1), "row pass");
-                check(cudaEventRecord(rows_done, stream_), "cudaEventRecord");
-                check(cudaStreamWaitEvent(cols_stream_, rows_done, 0), "wait");
-                check(ddmk::launch_spatial_warp<float>(sa, cols_stream_, 2), "column pass");
-                check(cudaEventRecord(cols_done, cols_stream_), "cudaEventRecord");
-                if (times) times->spatial_launches += 2;
-            }
-            check(cudaStreamWaitEvent(stream_, chunk_events_[2 * (chunks - 1) + 1], 0), "join");
-            sa.mid = d_mid;
-        } else {
-            for (int f0 = 0; f0 < N; f0 += F) {
-                sa.frame0 = f0;
-                sa.nframes = std::min(F, N - f0);
-                check(warp_s ? ddmk::launch_spatial_warp<float>(sa, stream_)
-                      : sp.f64 ? ddmk::launch_spatial<double>(sa, stream_)
-                               : ddmk::launch_spatial<float>(sa, stream_), "spatial kernels");
-                if (times) times->spatial_launches += 2;
-            }
-        }
+        spatial_pass(sa, sp.f64, warp_s, times);
         mark();
         spatial_passes += (uint64_t)N;
 
@@ -390,6 +403,92 @@ uint64_t Engine::run(const RunSpec& sp, PhaseTimes* times) {
         check(cudaStreamSynchronize(stream_), "sync");
     }
     return spatial_passes;
+}
+
+void Engine::spatial_shard(const void* d_frames, int pixel_bytes, int W, int H, int n, bool f64,
+                           void* d_spec, PhaseTimes* times) {
+    check(cudaSetDevice(device_), "cudaSetDevice");
+    const int sb = f64 ? 8 : 4;
+    // the warp spatial kernels write the same q-major layout as the generic ones
+    const bool warp_s = !f64 && ddmk::spatial_warp_supported(W, H, pixel_bytes, sb) &&
+                        std::getenv("DDM_B200_V1_SPATIAL") == nullptr;
+    ddmk::SpatialArgs sa = spatial_args(d_frames, pixel_bytes, W, H, n, f64);
+    sa.spec = d_spec;
+    sa.slot_of_flat = nullptr;
+    sa.layout.T = 1;
+    sa.layout.g_begin = 0;
+    sa.layout.g_count = (int64_t)H * (W / 2 + 1);
+    if (times) check(cudaEventRecord(ev_[0], stream_), "cudaEventRecord");
+    spatial_pass(sa, f64, warp_s, times);
+    if (times) {
+        check(cudaEventRecord(ev_[1], stream_), "cudaEventRecord");
+        check(cudaEventSynchronize(ev_[1]), "sync");
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ev_[0], ev_[1]);
+        times->spatial_ms += ms;
+    }
+}
+
+void Engine::temporal_segments(const void* d_recv, int64_t q_count, const std::vector<int>& seg_frames,
+                               bool f64, const std::vector<int64_t>& lags, void* d_out,
+                               int64_t out_stride, bool out_f64, PhaseTimes* times) {
+    check(cudaSetDevice(device_), "cudaSetDevice");
+    if (seg_frames.empty() || seg_frames.size() > (size_t)ddmk::SegTable::kMax)
+        throw std::invalid_argument("1 to 8 frame segments per sequence");
+    ddmk::SegTable segs;
+    segs.count = (int)seg_frames.size();
+    int N = 0;
+    for (int s = 0; s < segs.count; ++s) {
+        if (seg_frames[(size_t)s] < 1) throw std::invalid_argument("empty frame segment");
+        segs.n[s] = seg_frames[(size_t)s];
+        segs.off[s] = N;
+        segs.base[s] = q_count * (int64_t)N;
+        N += segs.n[s];
+    }
+    const int64_t N2 = pad_len(N);
+    const int sb = f64 ? 8 : 4;
+    const bool warp_t = use_warp_temporal(N, (int)N2, sb) && ddmk::temporal_warp_segments_ok(segs, N);
+    const int T = warp_t ? 1 : ddmk::temporal_tile(N, (int)N2, sb);
+    if (T == 0)
+        throw std::length_error("sequence of " + std::to_string(N) +
+                                " frames exceeds the single-CTA temporal engine");
+    ddmk::TemporalArgs ta;
+    ta.N = N;
+    ta.N2 = (int)N2;
+    ta.tw = {(int)N2, twiddles((int)N2, f64)};
+    ta.tw_half = {(int)N2 / 2, twiddles((int)N2 / 2, f64)};
+    ta.lag_index = upload_lags(lags, N);
+    ta.layout.T = T;
+    ta.layout.g_begin = 0;
+    ta.layout.g_count = q_count;
+    ta.out = d_out;
+    ta.out_f64 = out_f64 ? 1 : 0;
+    ta.out_stride = out_stride;
+    if (times) check(cudaEventRecord(ev_[2], stream_), "cudaEventRecord");
+    if (warp_t) {
+        ta.spec = d_recv;
+        ta.segs = segs;
+        check(ddmk::launch_temporal_warp(ta, num_sms_, stream_), "temporal kernel");
+    } else {
+        // generic engine: gather the segments into its tile-major layout first
+        const int64_t tiles = (q_count + T - 1) / T;
+        void* d_spec = spec_.ensure((size_t)tiles * N * T * 2 * sb);
+        check(f64 ? ddmk::launch_repack_segments<double>(d_recv, q_count, segs, N, T, d_spec, stream_)
+                  : ddmk::launch_repack_segments<float>(d_recv, q_count, segs, N, T, d_spec, stream_),
+              "repack kernel");
+        ta.spec = d_spec;
+        check(f64 ? ddmk::launch_temporal<double>(ta, stream_) : ddmk::launch_temporal<float>(ta, stream_),
+              "temporal kernel");
+        if (times) times->temporal_launches += 1;
+    }
+    if (times) {
+        times->temporal_launches += 1;
+        check(cudaEventRecord(ev_[3], stream_), "cudaEventRecord");
+        check(cudaEventSynchronize(ev_[3]), "sync");
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ev_[2], ev_[3]);
+        times->temporal_ms += ms;
+    }
 }
 
 void Engine::spectra(const void* d_frames, int pixel_bytes, int W, int H, int N, bool f64,

@@ -15,6 +15,8 @@
 
 #include <cuda_runtime.h>
 
+#include "kernels.cuh"
+
 namespace ddm::b200 {
 
 // CUDA failure (status 4 at the C-ABI).
@@ -94,6 +96,19 @@ public:
     void spectra(const void* d_frames, int pixel_bytes, int W, int H, int N, bool f64,
                  void* d_out);
 
+    // Sharded WITH_FT, step 1 on one rank: the rank's frame shard
+    // d_frames [n][H][W] -> d_spec [H*(W/2+1)][n] (every wave vector, q-major, working
+    // precision). Consecutive wave-vector ranges of d_spec are the all-to-all send blocks.
+    void spatial_shard(const void* d_frames, int pixel_bytes, int W, int H, int n, bool f64,
+                       void* d_spec, PhaseTimes* times = nullptr);
+
+    // Sharded WITH_FT, step 2 on one rank: q_count full sequences whose frames arrive as
+    // segments ([source][q][n_s] receive buffer, seg_frames[s] = n_s, sum = N) -> lag-major
+    // out[li * out_stride + q] for the requested lags (sorted, unique, within [0, N)).
+    void temporal_segments(const void* d_recv, int64_t q_count, const std::vector<int>& seg_frames,
+                           bool f64, const std::vector<int64_t>& lags, void* d_out,
+                           int64_t out_stride, bool out_f64, PhaseTimes* times = nullptr);
+
     // Device staging buffer for frames owned by the engine.
     void* frame_buffer(size_t bytes) { return frames_.ensure(bytes); }
     void* scratch(size_t bytes) { return user_scratch_.ensure(bytes); }
@@ -109,6 +124,12 @@ public:
     static Engine& instance(int device);
 
 private:
+    // Spatial passes over all frames of `sa` (frame chunks sized for L2), into sa.spec with
+    // layout sa.layout, ordered on stream_.
+    void spatial_pass(ddmk::SpatialArgs sa, bool f64, bool warp_s, PhaseTimes* times);
+    ddmk::SpatialArgs spatial_args(const void* d_frames, int pixel_bytes, int W, int H, int N,
+                                   bool f64);
+    const int* upload_lags(const std::vector<int64_t>& lags, int N);
     const void* twiddles(int len, bool f64);           // exp(-2 pi i j / len), j < len
     const void* post_twiddles(int W, bool f64);        // exp(-2 pi i k / W), k <= W/2
 

@@ -95,6 +95,24 @@ void emit(const ddm::ResultArchive& a, int64_t* out_lags, int64_t* out_n_lags,
     }
 }
 
+// Runs `fn` on the engine stream ordered after the caller's stream (cudaStream_t, may be
+// NULL), and orders the caller's stream after it.
+template <class Fn>
+void on_engine_stream(ddm::b200::Engine& eng, void* stream, Fn&& fn) {
+    cudaStream_t user = static_cast<cudaStream_t>(stream);
+    cudaEvent_t ev;
+    ddm::b200::check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+    struct Destroy {
+        cudaEvent_t e;
+        ~Destroy() { cudaEventDestroy(e); }
+    } guard{ev};
+    ddm::b200::check(cudaEventRecord(ev, user), "event record");
+    ddm::b200::check(cudaStreamWaitEvent(eng.stream(), ev, 0), "stream wait");
+    fn();
+    ddm::b200::check(cudaEventRecord(ev, eng.stream()), "event record");
+    ddm::b200::check(cudaStreamWaitEvent(user, ev, 0), "stream wait");
+}
+
 }  // namespace
 
 extern "C" {
@@ -246,6 +264,74 @@ int ddm_b200_run_device(const void* d_frames, int pixel_bytes, int width, int he
             if (spatial_ms) *spatial_ms = t.spatial_ms;
             if (temporal_ms) *temporal_ms = t.temporal_ms;
             if (kernel_launches) *kernel_launches = t.spatial_launches + t.temporal_launches;
+            return 0;
+        });
+    });
+}
+
+int ddm_b200_shard_plan(int64_t q_count, int64_t frames, int ranks, int64_t* frame_begin,
+                        int64_t* q_begin) {
+    return guarded([&] {
+        if (!frame_begin || !q_begin) throw ddm::InputError("null plan arrays");
+        const auto p = ddm::plan_shards(q_count, frames, ranks);
+        std::copy(p.frame_begin.begin(), p.frame_begin.end(), frame_begin);
+        std::copy(p.q_begin.begin(), p.q_begin.end(), q_begin);
+    });
+}
+
+int ddm_b200_spatial_shard_device(const void* d_frames, int pixel_bytes, int width, int height,
+                                  int frames, int precision, void* d_spec, int device,
+                                  void* stream, double* ms) {
+    return guarded([&] {
+        if (!d_frames || !d_spec) throw ddm::InputError("null device buffer");
+        if (pixel_bytes != 1 && pixel_bytes != 2) throw ddm::InputError("pixel_bytes must be 1 or 2");
+        if (width < 1 || height < 1 || frames < 1) throw ddm::InputError("dimensions must be positive");
+        ddm::detail::guard_device([&] {
+            auto& eng = ddm::b200::Engine::instance(device);
+            std::lock_guard<std::mutex> lock(eng.mutex());
+            on_engine_stream(eng, stream, [&] {
+                ddm::b200::PhaseTimes t;
+                eng.spatial_shard(d_frames, pixel_bytes, width, height, frames, precision != 0,
+                                  d_spec, ms ? &t : nullptr);
+                if (ms) *ms = t.spatial_ms;
+            });
+            return 0;
+        });
+    });
+}
+
+int ddm_b200_temporal_segments_device(const void* d_recv, int64_t q_count, int n_segments,
+                                      const int64_t* seg_frames, int precision,
+                                      const int64_t* lags, int64_t n_lags, void* d_out,
+                                      int64_t out_stride, int out_f64, int device, void* stream,
+                                      double* ms) {
+    return guarded([&] {
+        if (!d_recv || !d_out || !seg_frames) throw ddm::InputError("null buffer");
+        if (q_count < 1) throw ddm::InputError("need at least one wave vector");
+        if (n_segments < 1 || n_segments > 8) throw ddm::InputError("1 to 8 frame segments");
+        std::vector<int> segs((size_t)n_segments);
+        int64_t frames = 0;
+        for (int s = 0; s < n_segments; ++s) {
+            if (seg_frames[s] < 1) throw ddm::InputError("empty frame segment");
+            segs[(size_t)s] = (int)seg_frames[s];
+            frames += seg_frames[s];
+        }
+        const bool f64 = precision != 0;
+        if (frames > ddm::b200::max_frames(f64))
+            throw ddm::PlanError("sequence longer than the device temporal engine limit");
+        std::vector<int64_t> lag_list = (lags && n_lags > 0)
+                                            ? ddm::normalize_lags({lags, lags + n_lags}, frames)
+                                            : ddm::all_lags(frames);
+        if (out_stride < q_count) throw ddm::InputError("out_stride smaller than q_count");
+        ddm::detail::guard_device([&] {
+            auto& eng = ddm::b200::Engine::instance(device);
+            std::lock_guard<std::mutex> lock(eng.mutex());
+            on_engine_stream(eng, stream, [&] {
+                ddm::b200::PhaseTimes t;
+                eng.temporal_segments(d_recv, q_count, segs, f64, lag_list, d_out, out_stride,
+                                      out_f64 != 0, ms ? &t : nullptr);
+                if (ms) *ms = t.temporal_ms;
+            });
             return 0;
         });
     });

@@ -38,8 +38,21 @@ struct SpatialArgs {
     TwTable tw_row, tw_post, tw_col;    // row (W/2 or W), post (W), column (H)
 };
 
+// Sequences assembled from frame segments (the sharded corner turn): sequence
+// q of a group of q_count is the concatenation over s < count of
+//     spec + base[s] + q * n[s]      (n[s] complex values each; base[s] = q_count * off[s])
+// i.e. the receive buffer of the all-to-all, [source][q][frames of that source].
+struct SegTable {
+    static constexpr int kMax = 8;
+    int count = 0;                     // 0 = one contiguous segment of N (layout T = 1)
+    int n[kMax] = {};
+    int off[kMax] = {};                // frame offset of segment s within the sequence
+    int64_t base[kMax] = {};           // complex offset of segment s's [q][n[s]] block
+};
+
 struct TemporalArgs {
     const void* spec = nullptr;
+    SegTable segs;                     // warp engine only (the generic engine repacks first)
     int N = 0, N2 = 0;
     SpecLayout layout;
     TwTable tw;                        // length N2
@@ -61,10 +74,16 @@ cudaError_t launch_spatial(const SpatialArgs& a, cudaStream_t stream);
 template <typename S>
 cudaError_t launch_temporal(const TemporalArgs& a, cudaStream_t stream);
 
+// Segmented sequences (SegTable over q_count sequences) -> the engine's tile-major layout T.
+template <typename S>
+cudaError_t launch_repack_segments(const void* recv, int64_t q_count, const SegTable& segs, int N,
+                                   int T, void* spec, cudaStream_t stream);
+
 // Warp-per-sequence temporal engine (temporal_warp.cu): f32, N2 == 2048, wave-vector-major
 // spectra (layout T = 1).
 bool temporal_warp_supported(int N, int N2, int scalar_bytes);
 size_t temporal_warp_smem();
+bool temporal_warp_segments_ok(const SegTable& segs, int N);
 cudaError_t launch_temporal_warp(const TemporalArgs& a, int num_sms, cudaStream_t stream);
 
 // Register-resident spatial kernels (spatial_warp.cu): f32, power-of-two W/2 and H in

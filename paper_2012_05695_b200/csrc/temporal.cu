@@ -13,6 +13,7 @@
 // complex transform, then the standard real-input unfold. Every sequence is transformed on
 // its own, so results never depend on which wave vectors share a tile (cutoff and group
 // boundaries are bitwise invisible, as in the reference).
+#include <algorithm>
 #include <cstdlib>
 
 #include "kernels.cuh"
@@ -179,6 +180,50 @@ int temporal_threads(int, int) { return 256; }
 // (N2 = 16384 runs alone with 4 butterflies per thread). Prefer the largest T <= 8 whose
 // shared memory lets two CTAs share an SM (<= 113 KB) if that keeps T >= 4, otherwise the
 // largest T that fits one CTA. DDM_B200_TILE overrides (experiments).
+namespace {
+
+// recv [source s][q][n_s] -> spec tile-major [(q / T) * N + n][q % T]; one thread per output
+// element, consecutive threads walk q % T then n so stores are contiguous.
+template <typename S>
+__global__ void repack_segments_kernel(const cpx<S>* __restrict__ recv, int64_t q_count,
+                                       const __grid_constant__ SegTable segs, int N, int T,
+                                       cpx<S>* __restrict__ spec) {
+    const int64_t tiles = (q_count + T - 1) / T;
+    const int64_t total = tiles * N * T;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t tile = i / ((int64_t)N * T);
+        const int r = (int)(i - tile * N * T);
+        const int n = r / T, j = r - n * T;
+        const int64_t q = tile * T + j;
+        cpx<S> v = {S(0), S(0)};
+        if (q < q_count) {
+            int s = 0;
+            while (s + 1 < segs.count && n >= segs.off[s + 1]) ++s;
+            v = recv[segs.base[s] + q * segs.n[s] + (n - segs.off[s])];
+        }
+        spec[i] = v;
+    }
+}
+
+}  // namespace
+
+template <typename S>
+cudaError_t launch_repack_segments(const void* recv, int64_t q_count, const SegTable& segs, int N,
+                                   int T, void* spec, cudaStream_t stream) {
+    const int64_t total = (q_count + T - 1) / T * N * T;
+    const int blocks = (int)std::min<int64_t>(148 * 8, (total + 255) / 256);
+    if (blocks == 0) return cudaSuccess;
+    repack_segments_kernel<S><<<blocks, 256, 0, stream>>>(static_cast<const cpx<S>*>(recv), q_count,
+                                                          segs, N, T, static_cast<cpx<S>*>(spec));
+    return cudaGetLastError();
+}
+
+template cudaError_t launch_repack_segments<float>(const void*, int64_t, const SegTable&, int, int,
+                                                   void*, cudaStream_t);
+template cudaError_t launch_repack_segments<double>(const void*, int64_t, const SegTable&, int, int,
+                                                    void*, cudaStream_t);
+
 int temporal_tile(int N, int N2, int scalar_bytes) {
     auto ok = [&](int T, size_t cap) {
         const bool cap_bfly = (N2 > 8192) ? (T == 1) : (T * N2 <= 8192);

@@ -67,6 +67,21 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
         : "memory");
 }
 
+__device__ __forceinline__ void fence_expect(unsigned long long* bar, uint32_t bytes) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t bytes,
+                                          unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
+}
+
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t phase) {
     asm volatile(
         "{\n.reg .pred p;\nWAIT_%=:\n"
@@ -114,7 +129,7 @@ __device__ __forceinline__ void fft1024(cpx<float> (&v)[32], cpx<float>* scratch
 
 template <typename OutT, bool FULL, int kWarps>
 __global__ void __launch_bounds__(32 * kWarps, 1)
-temporal_warp_kernel(const cpx<float>* __restrict__ spec, int N_rt, int64_t nq,
+temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant__ SegTable segs, int N_rt, int64_t nq,
                      const int* __restrict__ lag_index, OutT* __restrict__ out,
                      int64_t out_stride, const int64_t* __restrict__ dest_of_slot,
                      double* __restrict__ corr_out, double* __restrict__ mean_out) {
@@ -157,8 +172,17 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, int N_rt, int64_t nq,
     const uint32_t bytes = (uint32_t)N * 8u;
     auto prefetch = [&](int64_t tile) {
         const int64_t q = tile * kWarps + warp;
-        if (lane == 0 && tile < ntiles && q < nq)
-            bulk_load(my.stage, spec + q * (int64_t)N, bytes, &my.bar);
+        if (lane == 0 && tile < ntiles && q < nq) {
+            if (segs.count == 0) {
+                bulk_load(my.stage, spec + q * (int64_t)N, bytes, &my.bar);
+            } else {
+                // sharded corner turn: one bulk copy per source segment, one transaction count
+                fence_expect(&my.bar, bytes);
+                for (int s = 0; s < segs.count; ++s)
+                    bulk_copy(my.stage + segs.off[s], spec + segs.base[s] + q * (int64_t)segs.n[s],
+                              (uint32_t)segs.n[s] * 8u, &my.bar);
+            }
+        }
     };
 
     uint32_t phase = 0u;
@@ -367,7 +391,7 @@ cudaError_t launch_w(const TemporalArgs& a, int num_sms, cudaStream_t stream) {
     const cpx<float>* spec = static_cast<const cpx<float>*>(a.spec);
     auto k = a.N == kL ? temporal_warp_kernel<OutT, true, W> : temporal_warp_kernel<OutT, false, W>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k<<<grid, 32 * W, smem, stream>>>(spec, a.N, a.layout.g_count, a.lag_index,
+    k<<<grid, 32 * W, smem, stream>>>(spec, a.segs, a.N, a.layout.g_count, a.lag_index,
                                       static_cast<OutT*>(a.out), a.out_stride, a.dest_of_slot,
                                       a.corr_out, a.mean_out);
     return cudaGetLastError();
@@ -379,8 +403,20 @@ size_t temporal_warp_smem() {
     return sizeof(WarpSmem) * tw_warps() + 2 * 32 * 32 * sizeof(cpx<float>) + kL * sizeof(float);
 }
 
+bool temporal_warp_segments_ok(const SegTable& segs, int N) {
+    if (segs.count < 0 || segs.count > SegTable::kMax) return false;
+    int total = 0;
+    for (int s = 0; s < segs.count; ++s) {
+        // bulk copies: 16-byte sizes, 16-byte aligned source and stage addresses
+        if (segs.n[s] < 1 || segs.n[s] % 2 || segs.off[s] != total || segs.base[s] % 2) return false;
+        total += segs.n[s];
+    }
+    return segs.count == 0 || total == N;
+}
+
 cudaError_t launch_temporal_warp(const TemporalArgs& a, int num_sms, cudaStream_t stream) {
     if (reinterpret_cast<uintptr_t>(a.spec) % 16 != 0) return cudaErrorMisalignedAddress;
+    if (!temporal_warp_segments_ok(a.segs, a.N)) return cudaErrorInvalidValue;
     if (tw_warps() == 8)
         return a.out_f64 ? launch_w<8, double>(a, num_sms, stream) : launch_w<8, float>(a, num_sms, stream);
     return a.out_f64 ? launch_w<12, double>(a, num_sms, stream) : launch_w<12, float>(a, num_sms, stream);

@@ -1,0 +1,190 @@
+"""Sharded WITH_FT over several GPUs of one node.
+
+One process per GPU. The reference is a single process whose out-of-core path slices the
+wave vectors into contiguous groups (`plan_with_ft`, `scheduler.cpp:365-384`) and loops all
+frames per group (`scheduler.cpp:89-171`). Here the two loops are split across ranks:
+
+  step 1  rank r transforms its frame shard [f_r, f_{r+1}) for every wave vector
+          (`ddm_b200_spatial_shard_device`): send buffer [Q][n_r], q-major, so the rows
+          [q_d, q_{d+1}) are the block for rank d;
+  corner  all-to-all (NCCL over NVLink via torch.distributed): rank d receives
+  turn    [source s][Q_d][n_s], the full sequences of its wave-vector slice in segments;
+  step 2  rank d runs the fused temporal engine over its slice, reading the segments in
+          place (`ddm_b200_temporal_segments_device`): lag-major [lags][Q_d], exactly the
+          reference's PartialResult of group d (`archive.hpp:48-61`).
+
+The map never crosses ranks: each rank keeps its partial in HBM (`assemble` gathers them for
+tests and host output, which is the reference's merge_partials).
+
+The compute steps are an injected `ops` object so the plan / exchange / assembly logic runs
+under `gloo` on CPU in the tests with a checker in place of the kernels; the product path is
+`DeviceOps`, which calls the C-ABI and has no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import ddm
+
+
+@dataclass(frozen=True)
+class ShardPlan:
+    """ddm::ShardPlan (include/ddm/scheduler.hpp): offsets with ranks + 1 entries each."""
+    ranks: int
+    frames: int
+    q_count: int
+    frame_begin: tuple
+    q_begin: tuple
+
+    def frames_of(self, r: int) -> int:
+        return self.frame_begin[r + 1] - self.frame_begin[r]
+
+    def q_of(self, r: int) -> int:
+        return self.q_begin[r + 1] - self.q_begin[r]
+
+    def send_counts(self, r: int) -> List[int]:
+        """complex values rank r sends to each destination (its frames x their slice)."""
+        return [self.q_of(d) * self.frames_of(r) for d in range(self.ranks)]
+
+    def recv_counts(self, r: int) -> List[int]:
+        """complex values rank r receives from each source (its slice x their frames)."""
+        return [self.q_of(r) * self.frames_of(s) for s in range(self.ranks)]
+
+
+def plan_shards(q_count: int, frames: int, ranks: int) -> ShardPlan:
+    """ddm::plan_shards through the C-ABI (host-only; no device needed)."""
+    fb = np.zeros(ranks + 1, dtype=np.int64)
+    qb = np.zeros(ranks + 1, dtype=np.int64)
+    ddm._check(ddm.lib().ddm_b200_shard_plan(C.c_int64(q_count), C.c_int64(frames), int(ranks),
+                                             ddm._p(fb, C.c_int64), ddm._p(qb, C.c_int64)))
+    return ShardPlan(int(ranks), int(frames), int(q_count), tuple(int(x) for x in fb),
+                     tuple(int(x) for x in qb))
+
+
+class DeviceOps:
+    """The product compute steps: C-ABI kernels on the rank's GPU (torch tensors as HBM)."""
+
+    def __init__(self, width: int, height: int, precision: str = "f32", device: int = 0,
+                 pixel_bytes: int = 2, timing: bool = True):
+        self.width, self.height = width, height
+        self.timing = timing  # per-step device times (synchronises the host per step)
+        self.precision = precision
+        self.device = device
+        self.pixel_bytes = pixel_bytes
+        self.spatial_ms = 0.0
+        self.temporal_ms = 0.0
+
+    def _stream(self):
+        import torch
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def spatial(self, frames_local, n_local: int, send) -> None:
+        """frames_local: device tensor of the shard's pixels; send: device tensor of
+        Q * n_local complex values (real pairs)."""
+        ms = C.c_double(0.0)
+        ddm._check(ddm.lib().ddm_b200_spatial_shard_device(
+            C.c_void_p(frames_local.data_ptr()), self.pixel_bytes, self.width, self.height,
+            int(n_local), 0 if self.precision == "f32" else 1, C.c_void_p(send.data_ptr()),
+            self.device, C.c_void_p(self._stream()), C.byref(ms) if self.timing else None))
+        self.spatial_ms = ms.value
+
+    def temporal(self, recv, q_count: int, seg_frames: Sequence[int], out, out_stride: int,
+                 lags: Optional[Sequence[int]] = None, out_f64: bool = False) -> None:
+        segs = np.ascontiguousarray(np.asarray(seg_frames, dtype=np.int64))
+        lag_arr = np.ascontiguousarray(np.asarray(lags if lags is not None else [], dtype=np.int64))
+        ms = C.c_double(0.0)
+        ddm._check(ddm.lib().ddm_b200_temporal_segments_device(
+            C.c_void_p(recv.data_ptr()), C.c_int64(q_count), len(segs), ddm._p(segs, C.c_int64),
+            0 if self.precision == "f32" else 1,
+            ddm._p(lag_arr, C.c_int64) if len(lag_arr) else None, C.c_int64(len(lag_arr)),
+            C.c_void_p(out.data_ptr()), C.c_int64(out_stride), 1 if out_f64 else 0, self.device,
+            C.c_void_p(self._stream()), C.byref(ms) if self.timing else None))
+        self.temporal_ms = ms.value
+
+
+class ShardedRun:
+    """One rank of a sharded WITH_FT run. Buffers are allocated once and reused per step.
+
+    Scalars travel as real pairs: f32 runs exchange float32 tensors, f64 runs float64.
+    """
+
+    def __init__(self, plan: ShardPlan, rank: int, width: int, height: int, ops, *,
+                 precision: str = "f32", device=None, group=None, lags=None,
+                 out_f64: bool = False):
+        import torch
+        self.torch = torch
+        self.plan, self.rank = plan, rank
+        self.width, self.height = width, height
+        if plan.q_count != height * (width // 2 + 1):
+            raise ddm.InputError("plan q_count must be the half-plane size H*(W/2+1)")
+        self.ops, self.group = ops, group
+        self.precision = precision
+        self.lags = None if lags is None else [int(x) for x in lags]
+        self.n_lags = plan.frames if lags is None else len(self.lags)
+        self.out_f64 = out_f64
+        real = torch.float32 if precision == "f32" else torch.float64
+        dev = torch.device("cpu") if device is None else torch.device(device)
+        Q, n_r = plan.q_count, plan.frames_of(rank)
+        self.send = torch.empty(2 * Q * n_r, dtype=real, device=dev)
+        # one rank: the send buffer already is the single-source receive buffer
+        self.recv = (self.send if plan.ranks == 1 else
+                     torch.empty(2 * plan.q_of(rank) * plan.frames, dtype=real, device=dev))
+        self.out = torch.empty(self.n_lags * max(plan.q_of(rank), 1),
+                               dtype=torch.float64 if out_f64 else torch.float32, device=dev)
+        self.send_splits = [2 * c for c in plan.send_counts(rank)]
+        self.recv_splits = [2 * c for c in plan.recv_counts(rank)]
+        self.seg_frames = [plan.frames_of(s) for s in range(plan.ranks)]
+
+    def exchange(self) -> None:
+        """The corner turn: every rank's [Q_d][n_r] block to rank d."""
+        if self.plan.ranks == 1:
+            return
+        import torch.distributed as dist
+        dist.all_to_all_single(self.recv, self.send, self.recv_splits, self.send_splits,
+                               group=self.group)
+
+    def step(self, frames_local):
+        """Whole sharded pass for this rank; returns the rank's lag-major partial
+        [n_lags][Q_r] (a view of `self.out`)."""
+        self.ops.spatial(frames_local, self.plan.frames_of(self.rank), self.send)
+        self.exchange()
+        q_r = self.plan.q_of(self.rank)
+        if q_r > 0:
+            self.ops.temporal(self.recv, q_r, self.seg_frames, self.out, q_r, lags=self.lags,
+                              out_f64=self.out_f64)
+        return self.out[: self.n_lags * q_r].view(self.n_lags, q_r)
+
+
+def assemble(plan: ShardPlan, partials: Sequence[np.ndarray]) -> np.ndarray:
+    """merge_partials over the ranks' outputs (`scheduler.cpp:485-542` with identity flat
+    positions): [n_lags][Q] from the per-rank [n_lags][Q_r] blocks."""
+    blocks = [np.asarray(p) for p in partials]
+    n_lags = blocks[0].shape[0]
+    out = np.zeros((n_lags, plan.q_count), dtype=np.float64)
+    for r, b in enumerate(blocks):
+        if b.shape != (n_lags, plan.q_of(r)):
+            raise ddm.InputError(f"partial of rank {r} has shape {b.shape}, "
+                                 f"expected {(n_lags, plan.q_of(r))}")
+        out[:, plan.q_begin[r]:plan.q_begin[r + 1]] = b
+    return out
+
+
+def gather_partials(plan: ShardPlan, partial, rank: int, group=None):
+    """Collect every rank's partial on rank 0 (host numpy), None elsewhere."""
+    import torch
+    import torch.distributed as dist
+    if plan.ranks == 1:
+        return [partial.detach().cpu().numpy()]
+    n_lags = partial.shape[0]
+    width = max(plan.q_of(r) for r in range(plan.ranks))
+    padded = torch.zeros(n_lags, width, dtype=partial.dtype, device=partial.device)
+    padded[:, : partial.shape[1]] = partial
+    bufs = [torch.zeros_like(padded) for _ in range(plan.ranks)] if rank == 0 else None
+    dist.gather(padded, bufs, dst=0, group=group)
+    if rank != 0:
+        return None
+    return [b[:, : plan.q_of(r)].cpu().numpy() for r, b in enumerate(bufs)]
