@@ -89,17 +89,25 @@ rows2_kernel(const Pix* __restrict__ frames, int H, int frame0, const cpx<S>* __
     __syncthreads();
 
     // even/odd split: X[c] = (Z[c] + conj Z[L-c]) / 2 + W_W^c (Z[c] - conj Z[L-c]) / (2i)
+    // thread (rr, cb) owns row rr and the columns c = cb + CS j: fixed strides, no division,
+    // all twiddle loads hoisted by the unrolled loop
+    constexpr int CS = kThreads / RB;                // column stride
+    constexpr int NJ = (Wh + CS - 1) / CS;
     const S half = S(0.5);
-    cpx<S>* dst = mid + (size_t)fi * Wh * H + r0;
-    for (int idx = threadIdx.x; idx < nr * Wh; idx += kThreads) {
-        const int c = idx / nr, rr = idx - c * nr;
-        const cpx<S>* z = region_base + rr * REG;
-        const cpx<S> zk = z[c % L];
-        cpx<S> zc = z[(L - c) % L];
+    const int rr = threadIdx.x % RB, cb = threadIdx.x / RB;
+    const cpx<S>* z = region_base + rr * REG;
+    cpx<S>* dst = mid + (size_t)fi * Wh * H + r0 + rr + (size_t)cb * H;
+    const size_t step = (size_t)CS * H;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+        const int c = cb + CS * j;
+        if (j == NJ - 1 && c >= Wh) break;
+        const cpx<S> zk = z[c < L ? c : c - L];
+        cpx<S> zc = z[c == 0 ? 0 : L - c];
         zc.y = -zc.y;
         const cpx<S> e = {(zk.x + zc.x) * half, (zk.y + zc.y) * half};
         const cpx<S> o = {(zk.y - zc.y) * half, -(zk.x - zc.x) * half};
-        dst[(size_t)c * H + rr] = cadd(e, cmul(tw_post[c], o));
+        dst[j * step] = cadd(e, cmul(tw_post[c], o));
     }
 }
 
@@ -142,6 +150,20 @@ cols2_kernel(const cpx<S>* __restrict__ mid, int Wh, int N, int frame0, int nfra
     __syncthreads();
 
     const int n0 = frame0 + f0;
+    const int64_t plane = (int64_t)HL * Wh;
+    if (!slot_of_flat && lay.g_begin == 0 && lay.g_count == plane) {
+        // every wave vector of the plane, identity slots: thread (f, rb + RS j) copies one
+        // frame of wave vector (r, c); consecutive threads fill F-frame runs
+        constexpr int RS = kThreads / F;             // row stride
+        const int f = threadIdx.x % F, rb = threadIdx.x / F;
+        if (f < nf) {
+            cpx<S>* dst = spec + ((int64_t)rb * Wh + c) * N + n0 + f;
+            const int64_t step = (int64_t)RS * Wh * N;
+#pragma unroll 8
+            for (int j = 0; j < HL / RS; ++j) dst[j * step] = sm[(rb + RS * j) * SP + f];
+        }
+        return;
+    }
     for (int idx = threadIdx.x; idx < HL * F; idx += kThreads) {
         const int r = idx / F, f = idx - r * F;
         if (f >= nf) continue;
