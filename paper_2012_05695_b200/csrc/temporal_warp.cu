@@ -42,6 +42,7 @@ __device__ __forceinline__ int padded(int n) { return n + (n >> 5); }
 struct WarpSmem {
     cpx<float> stage[kPad];
     cpx<float> scratch[kPad];
+    float pw[kPad];              // |t|^2, then S(m): frees the stage for the next copy early
     unsigned long long bar;
     unsigned long long pad_;
 };
@@ -127,7 +128,9 @@ __device__ __forceinline__ void fft1024(cpx<float> (&v)[32], cpx<float>* scratch
     RegDft<32, SIGN, float>::run(v);
 }
 
-template <typename OutT, bool FULL, int kWarps>
+// kDiag: the batched SequenceEngine API's extra outputs (corr, mean); compiled out of the
+// run path so none of its predicated f64 work is issued there.
+template <typename OutT, bool FULL, bool kDiag, int kWarps>
 __global__ void __launch_bounds__(32 * kWarps, 1)
 temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant__ SegTable segs, int N_rt, int64_t nq,
                      const int* __restrict__ lag_index, OutT* __restrict__ out,
@@ -143,7 +146,6 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     WarpSmem& my = ws[warp];
-    float* stf = reinterpret_cast<float*>(my.stage);    // f32 views
     float* scf = reinterpret_cast<float*>(my.scratch);
 
     for (int m = threadIdx.x; m < N; m += blockDim.x) rcp[m] = (float)(1.0 / (double)(N - m));
@@ -166,6 +168,9 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
         base_unf = {(float)cs, (float)sn};
     }
     const float inv_nf = 1.0f / (float)N;
+    // 16-byte vector stores of whole tiles: f32 map, aligned base and row stride
+    const bool vec_store = sizeof(OutT) == 4 && kWarps % 4 == 0 &&
+                           ((uintptr_t)out & 15) == 0 && (out_stride & 3) == 0;
     __syncthreads();
 
     const int64_t ntiles = (nq + kWarps - 1) / kWarps;
@@ -254,9 +259,11 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
             v[b] = x;
         }
         __syncwarp();
+        // the stage is free: start the next sequence's copy (it lands during three FFTs)
+        prefetch(tile + gridDim.x);
 #pragma unroll
         for (int b = 0; b < 32; ++b)
-            stf[padded(lane + 32 * b)] = v[b].x * v[b].x + v[b].y * v[b].y;
+            my.pw[padded(lane + 32 * b)] = v[b].x * v[b].x + v[b].y * v[b].y;
         fft1024<-1, true>(v, my.scratch, lane, tw_odd);
 #pragma unroll
         for (int d = 0; d < 32; ++d) v[d] = {pe[d], v[d].x * v[d].x + v[d].y * v[d].y};
@@ -272,7 +279,7 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
                 const int n = 32 * lane + j;
-                qv[j] = (n < N) ? stf[padded(n)] + stf[padded(N - 1 - n)] : 0.f;
+                qv[j] = (n < N) ? my.pw[padded(n)] + my.pw[padded(N - 1 - n)] : 0.f;
             }
             float r = 0.f;
 #pragma unroll
@@ -288,7 +295,7 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
             }
             const float base = (float)(incl - (double)r);
             __syncwarp();
-            float* sarea = stf + kPad;  // second half of the stage
+            float* sarea = my.pw;  // S(m) replaces |t|^2
 #pragma unroll
             for (int j = 0; j < 32; ++j) sarea[padded(32 * lane + j)] = qv[j] + base;
             __syncwarp();
@@ -296,8 +303,6 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
             for (int d = 0; d < 32; ++d) sv[d] = sarea[padded(lane + 32 * d)];
             __syncwarp();
         }
-        // the stage is free: start the next sequence's copy
-        prefetch(tile + gridDim.x);
 
         // ---- unfold + combine on the lane's own m = c + 32 d; U[L - m] sits in lane
         //      (32 - c) mod 32, register 31 - d (lane 0: its own register (32 - d) mod 32)
@@ -318,35 +323,39 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
             if (m < N) {
                 const float val = fmaf(-re2, inv_n2, sv[d]) * rcp[m];
                 scf[padded(m)] = (m == 0) ? 0.f : val;
-                if (corr_out && live) corr_out[q * N + m] = 0.5 * (double)re2 / (double)kN2;
+                if constexpr (kDiag)
+                    if (corr_out && live) corr_out[q * N + m] = 0.5 * (double)re2 / (double)kN2;
             }
         }
-        if (mean_out && live && lane == 0) {
+        if (kDiag && mean_out && live && lane == 0) {
             mean_out[2 * q] = (double)mx;
             mean_out[2 * q + 1] = (double)my_;
         }
 
-        // ---- tile store: lag rows of 12 consecutive wave vectors (48 B runs)
+        // ---- tile store: lag rows of kWarps consecutive wave vectors (32 B runs for f32)
         __syncthreads();
         const int64_t q0 = tile * kWarps;
         if (!lag_index && !dest_of_slot && q0 + kWarps <= nq) {
-            for (int m = threadIdx.x; m < N; m += blockDim.x) {
-                OutT vv[kWarps];
+            OutT* dst = out + (int64_t)threadIdx.x * out_stride + q0;
+            const int64_t step = (int64_t)blockDim.x * out_stride;
+            if (vec_store) {
+#pragma unroll 2
+                for (int m = threadIdx.x; m < N; m += blockDim.x, dst += step) {
+                    float vv[kWarps];
 #pragma unroll
-                for (int j = 0; j < kWarps; ++j)
-                    vv[j] = (OutT) reinterpret_cast<const float*>(ws[j].scratch)[padded(m)];
-                OutT* dst = out + (int64_t)m * out_stride + q0;
-                if constexpr (sizeof(OutT) == 4) {
-                    if (((uintptr_t)dst & 15) == 0) {
+                    for (int j = 0; j < kWarps; ++j)
+                        vv[j] = reinterpret_cast<const float*>(ws[j].scratch)[padded(m)];
 #pragma unroll
-                        for (int k = 0; k < kWarps / 4; ++k)
-                            reinterpret_cast<float4*>(dst)[k] =
-                                make_float4(vv[4 * k], vv[4 * k + 1], vv[4 * k + 2], vv[4 * k + 3]);
-                        continue;
-                    }
+                    for (int k = 0; k < kWarps / 4; ++k)
+                        reinterpret_cast<float4*>(dst)[k] =
+                            make_float4(vv[4 * k], vv[4 * k + 1], vv[4 * k + 2], vv[4 * k + 3]);
                 }
+            } else {
+                for (int m = threadIdx.x; m < N; m += blockDim.x, dst += step) {
 #pragma unroll
-                for (int j = 0; j < kWarps; ++j) dst[j] = vv[j];
+                    for (int j = 0; j < kWarps; ++j)
+                        dst[j] = (OutT) reinterpret_cast<const float*>(ws[j].scratch)[padded(m)];
+                }
             }
         } else {
             for (int idx = threadIdx.x; idx < N * kWarps; idx += blockDim.x) {
@@ -372,24 +381,18 @@ bool temporal_warp_supported(int N, int N2, int scalar_bytes) {
 
 namespace {
 
-// warps (wave vectors) per CTA: 8 (255 registers, no spills); DDM_TW_WARPS=12 selects the
-// 12-warp build (168 registers) for A/B runs
-int tw_warps() {
-    static const int w = [] {
-        const char* e = std::getenv("DDM_TW_WARPS");
-        return (e && std::atoi(e) == 12) ? 12 : 8;
-    }();
-    return w;
-}
+// 8 warps (wave vectors) per CTA: 255 registers without spills, one CTA per SM
+constexpr int kTW = 8;
 
-template <int W, typename OutT>
+template <typename OutT, bool kDiag>
 cudaError_t launch_w(const TemporalArgs& a, int num_sms, cudaStream_t stream) {
+    constexpr int W = kTW;
     const size_t smem = sizeof(WarpSmem) * W + 2 * 32 * 32 * sizeof(cpx<float>) + kL * sizeof(float);
     const int64_t tiles = (a.layout.g_count + W - 1) / W;
     const int grid = (int)std::min<int64_t>(tiles, (int64_t)num_sms);
     if (grid == 0) return cudaSuccess;
     const cpx<float>* spec = static_cast<const cpx<float>*>(a.spec);
-    auto k = a.N == kL ? temporal_warp_kernel<OutT, true, W> : temporal_warp_kernel<OutT, false, W>;
+    auto k = a.N == kL ? temporal_warp_kernel<OutT, true, kDiag, W> : temporal_warp_kernel<OutT, false, kDiag, W>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k<<<grid, 32 * W, smem, stream>>>(spec, a.segs, a.N, a.layout.g_count, a.lag_index,
                                       static_cast<OutT*>(a.out), a.out_stride, a.dest_of_slot,
@@ -400,7 +403,7 @@ cudaError_t launch_w(const TemporalArgs& a, int num_sms, cudaStream_t stream) {
 }  // namespace
 
 size_t temporal_warp_smem() {
-    return sizeof(WarpSmem) * tw_warps() + 2 * 32 * 32 * sizeof(cpx<float>) + kL * sizeof(float);
+    return sizeof(WarpSmem) * kTW + 2 * 32 * 32 * sizeof(cpx<float>) + kL * sizeof(float);
 }
 
 bool temporal_warp_segments_ok(const SegTable& segs, int N) {
@@ -417,9 +420,11 @@ bool temporal_warp_segments_ok(const SegTable& segs, int N) {
 cudaError_t launch_temporal_warp(const TemporalArgs& a, int num_sms, cudaStream_t stream) {
     if (reinterpret_cast<uintptr_t>(a.spec) % 16 != 0) return cudaErrorMisalignedAddress;
     if (!temporal_warp_segments_ok(a.segs, a.N)) return cudaErrorInvalidValue;
-    if (tw_warps() == 8)
-        return a.out_f64 ? launch_w<8, double>(a, num_sms, stream) : launch_w<8, float>(a, num_sms, stream);
-    return a.out_f64 ? launch_w<12, double>(a, num_sms, stream) : launch_w<12, float>(a, num_sms, stream);
+    if (a.corr_out || a.mean_out) {
+        if (!a.out_f64) return cudaErrorInvalidValue;
+        return launch_w<double, true>(a, num_sms, stream);
+    }
+    return a.out_f64 ? launch_w<double, false>(a, num_sms, stream) : launch_w<float, false>(a, num_sms, stream);
 }
 
 }  // namespace ddmk
