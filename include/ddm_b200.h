@@ -125,6 +125,18 @@ int ddm_b200_spatial_shard_device(const void* d_frames, int pixel_bytes, int wid
                                   int frames, int precision, void* d_spec, int device,
                                   void* stream, double* ms);
 
+/* Step 1 fused with the corner turn (NVLink peer stores): as spatial_shard_device, but wave
+   vector k of this rank's frames is stored straight into its owner's receive buffer,
+   dest[d] + (k - q_begin[d]) * frames for q_begin[d] <= k < q_begin[d+1], where dest[d] is a
+   device pointer valid on this GPU (a peer mapping of rank d's buffer, already offset to this
+   rank's segment).  Needs the register-resident spatial kernels (f32, power-of-two W/2 and
+   H <= 1024); status 1 otherwise.  The caller orders the peers' step 2 after every rank's
+   step 1 (a cross-GPU barrier). */
+int ddm_b200_spatial_shard_p2p_device(const void* d_frames, int pixel_bytes, int width, int height,
+                                      int frames, int precision, int ranks,
+                                      const int64_t* q_begin, void* const* dest, int device,
+                                      void* stream, double* ms);
+
 /* Step 2 on one rank, replacing the per-sequence loop (scheduler.cpp:146-162) for its group:
    d_recv is the all-to-all receive buffer, [source s][q_count][seg_frames[s]] complex;
    sequence q is the concatenation of its source segments.  Writes the lag-major map

@@ -406,7 +406,7 @@ uint64_t Engine::run(const RunSpec& sp, PhaseTimes* times) {
 }
 
 void Engine::spatial_shard(const void* d_frames, int pixel_bytes, int W, int H, int n, bool f64,
-                           void* d_spec, PhaseTimes* times) {
+                           void* d_spec, PhaseTimes* times, const ddmk::PeerTable* peers) {
     check(cudaSetDevice(device_), "cudaSetDevice");
     const int sb = f64 ? 8 : 4;
     // the warp spatial kernels write the same q-major layout as the generic ones
@@ -418,6 +418,12 @@ void Engine::spatial_shard(const void* d_frames, int pixel_bytes, int W, int H, 
     sa.layout.T = 1;
     sa.layout.g_begin = 0;
     sa.layout.g_count = (int64_t)H * (W / 2 + 1);
+    if (peers && peers->ranks > 0) {
+        if (!warp_s)
+            throw std::invalid_argument("the fused NVLink corner turn needs the register-resident "
+                                        "spatial kernels (f32, power-of-two W/2 and H <= 1024)");
+        sa.peers = *peers;
+    }
     if (times) check(cudaEventRecord(ev_[0], stream_), "cudaEventRecord");
     spatial_pass(sa, f64, warp_s, times);
     if (times) {

@@ -99,8 +99,12 @@ public:
     // Sharded WITH_FT, step 1 on one rank: the rank's frame shard
     // d_frames [n][H][W] -> d_spec [H*(W/2+1)][n] (every wave vector, q-major, working
     // precision). Consecutive wave-vector ranges of d_spec are the all-to-all send blocks.
+    // With `peers` (ranks > 0) the column pass stores straight into the owners' receive
+    // buffers (fused NVLink corner turn; register-resident spatial kernels only) and d_spec
+    // is unused.
     void spatial_shard(const void* d_frames, int pixel_bytes, int W, int H, int n, bool f64,
-                       void* d_spec, PhaseTimes* times = nullptr);
+                       void* d_spec, PhaseTimes* times = nullptr,
+                       const ddmk::PeerTable* peers = nullptr);
 
     // Sharded WITH_FT, step 2 on one rank: q_count full sequences whose frames arrive as
     // segments ([source][q][n_s] receive buffer, seg_frames[s] = n_s, sum = N) -> lag-major

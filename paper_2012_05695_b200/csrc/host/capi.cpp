@@ -300,6 +300,44 @@ int ddm_b200_spatial_shard_device(const void* d_frames, int pixel_bytes, int wid
     });
 }
 
+int ddm_b200_spatial_shard_p2p_device(const void* d_frames, int pixel_bytes, int width, int height,
+                                      int frames, int precision, int ranks,
+                                      const int64_t* q_begin, void* const* dest, int device,
+                                      void* stream, double* ms) {
+    return guarded([&] {
+        if (!d_frames || !q_begin || !dest) throw ddm::InputError("null buffer");
+        if (pixel_bytes != 1 && pixel_bytes != 2) throw ddm::InputError("pixel_bytes must be 1 or 2");
+        if (width < 1 || height < 1 || frames < 1) throw ddm::InputError("dimensions must be positive");
+        if (ranks < 1 || ranks > ddmk::PeerTable::kMax) throw ddm::InputError("ranks must be in [1, 8]");
+        ddmk::PeerTable peers;
+        peers.ranks = ranks;
+        const int64_t plane = int64_t(height) * (width / 2 + 1);
+        for (int d = 0; d <= ranks; ++d) peers.q_begin[d] = q_begin[d];
+        if (peers.q_begin[0] != 0 || peers.q_begin[ranks] != plane)
+            throw ddm::InputError("q_begin must cover the half plane");
+        for (int d = 0; d < ranks; ++d) {
+            if (peers.q_begin[d + 1] < peers.q_begin[d]) throw ddm::InputError("q_begin must ascend");
+            if (!dest[d] && peers.q_begin[d + 1] > peers.q_begin[d]) throw ddm::InputError("null destination");
+            peers.base[d] = dest[d];
+        }
+        ddm::detail::guard_device([&] {
+            auto& eng = ddm::b200::Engine::instance(device);
+            std::lock_guard<std::mutex> lock(eng.mutex());
+            on_engine_stream(eng, stream, [&] {
+                ddm::b200::PhaseTimes t;
+                try {
+                    eng.spatial_shard(d_frames, pixel_bytes, width, height, frames, precision != 0,
+                                      nullptr, ms ? &t : nullptr, &peers);
+                } catch (const std::invalid_argument& e) {
+                    throw ddm::InputError(e.what());
+                }
+                if (ms) *ms = t.spatial_ms;
+            });
+            return 0;
+        });
+    });
+}
+
 int ddm_b200_temporal_segments_device(const void* d_recv, int64_t q_count, int n_segments,
                                       const int64_t* seg_frames, int precision,
                                       const int64_t* lags, int64_t n_lags, void* d_out,

@@ -26,6 +26,17 @@ struct SpecLayout {
     int64_t tiles() const { return (g_count + T - 1) / T; }
 };
 
+// Fused corner turn over NVLink: the column pass stores wave vector k of the
+// shard's frames straight into the receive buffer of the rank that owns k,
+//     base[d] + (k - q_begin[d]) * N + n     for q_begin[d] <= k < q_begin[d + 1]
+// (base[d] = that rank's receive buffer + this rank's segment offset, a peer pointer).
+struct PeerTable {
+    static constexpr int kMax = 8;
+    int ranks = 0;                     // 0 = local spectra (spec / layout)
+    int64_t q_begin[kMax + 1] = {};
+    void* base[kMax] = {};
+};
+
 struct SpatialArgs {
     const void* frames = nullptr;  // [N][H][W] pixels
     int pixel_bytes = 2;           // 2 u16, 1 u8, 4 f32, 8 f64 (real-valued frames)
@@ -35,6 +46,7 @@ struct SpatialArgs {
     void* spec = nullptr;
     SpecLayout layout;
     const int* slot_of_flat = nullptr;  // nullable: flat (row*(W/2+1)+col) -> retained index
+    PeerTable peers;                    // register-resident kernels only
     TwTable tw_row, tw_post, tw_col;    // row (W/2 or W), post (W), column (H)
 };
 

@@ -116,7 +116,7 @@ template <typename S, int HL>
 __global__ void __launch_bounds__(kThreads)
 cols2_kernel(const cpx<S>* __restrict__ mid, int Wh, int N, int frame0, int nframes,
              const cpx<S>* __restrict__ tw_col, cpx<S>* __restrict__ spec, SpecLayout lay,
-             const int* __restrict__ slot_of_flat) {
+             const int* __restrict__ slot_of_flat, const __grid_constant__ PeerTable peers) {
     constexpr int A = split_a<HL>(), B = HL / A;
     constexpr int F = kThreads / A;                  // frames per CTA (one per group)
     constexpr int REG = B * (A + 1);
@@ -151,6 +151,23 @@ cols2_kernel(const cpx<S>* __restrict__ mid, int Wh, int N, int frame0, int nfra
 
     const int n0 = frame0 + f0;
     const int64_t plane = (int64_t)HL * Wh;
+    if (peers.ranks > 0) {
+        // fused corner turn: every wave vector goes to its owner's receive buffer (a peer
+        // pointer over NVLink); rows ascend with j, so the owner index only moves forward
+        constexpr int RS = kThreads / F;
+        const int f = threadIdx.x % F, rb = threadIdx.x / F;
+        if (f < nf) {
+            int d = 0;
+#pragma unroll 4
+            for (int j = 0; j < HL / RS; ++j) {
+                const int64_t k = (int64_t)(rb + RS * j) * Wh + c;
+                while (d + 1 < peers.ranks && k >= peers.q_begin[d + 1]) ++d;
+                cpx<S>* dst = static_cast<cpx<S>*>(peers.base[d]);
+                dst[(k - peers.q_begin[d]) * N + n0 + f] = sm[(rb + RS * j) * SP + f];
+            }
+        }
+        return;
+    }
     if (!slot_of_flat && lay.g_begin == 0 && lay.g_count == plane) {
         // every wave vector of the plane, identity slots: thread (f, rb + RS j) copies one
         // frame of wave vector (r, c); consecutive threads fill F-frame runs
@@ -212,7 +229,7 @@ void launch_cols2(const SpatialArgs& a, cudaStream_t st) {
     k<<<grid, kThreads, smem, st>>>(static_cast<const cpx<S>*>(a.mid), Wh, a.N, a.frame0,
                                     a.nframes, static_cast<const cpx<S>*>(a.tw_col.ptr),
                                     static_cast<cpx<S>*>(a.spec), a.layout,
-                                    a.slot_of_flat);
+                                    a.slot_of_flat, a.peers);
 }
 
 bool pow2_in(int x, int lo, int hi) { return x >= lo && x <= hi && (x & (x - 1)) == 0; }

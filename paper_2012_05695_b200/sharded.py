@@ -92,6 +92,20 @@ class DeviceOps:
             self.device, C.c_void_p(self._stream()), C.byref(ms) if self.timing else None))
         self.spatial_ms = ms.value
 
+    def spatial_p2p(self, frames_local, n_local: int, q_begin: Sequence[int],
+                    dest: Sequence[int]) -> None:
+        """Step 1 fused with the corner turn: the column pass stores every wave vector of
+        the shard straight into its owner's receive buffer (`dest[d]`, device pointers valid
+        on this GPU: peer mappings over NVLink, already offset to this rank's segment)."""
+        qb = np.ascontiguousarray(np.asarray(q_begin, dtype=np.int64))
+        ptrs = (C.c_void_p * len(dest))(*[C.c_void_p(int(x)) for x in dest])
+        ms = C.c_double(0.0)
+        ddm._check(ddm.lib().ddm_b200_spatial_shard_p2p_device(
+            C.c_void_p(frames_local.data_ptr()), self.pixel_bytes, self.width, self.height,
+            int(n_local), 0 if self.precision == "f32" else 1, len(dest), ddm._p(qb, C.c_int64),
+            ptrs, self.device, C.c_void_p(self._stream()), C.byref(ms) if self.timing else None))
+        self.spatial_ms = ms.value
+
     def temporal(self, recv, q_count: int, seg_frames: Sequence[int], out, out_stride: int,
                  lags: Optional[Sequence[int]] = None, out_f64: bool = False) -> None:
         segs = np.ascontiguousarray(np.asarray(seg_frames, dtype=np.int64))
@@ -114,7 +128,7 @@ class ShardedRun:
 
     def __init__(self, plan: ShardPlan, rank: int, width: int, height: int, ops, *,
                  precision: str = "f32", device=None, group=None, lags=None,
-                 out_f64: bool = False):
+                 out_f64: bool = False, exchange: str = "nccl"):
         import torch
         self.torch = torch
         self.plan, self.rank = plan, rank
@@ -129,18 +143,50 @@ class ShardedRun:
         real = torch.float32 if precision == "f32" else torch.float64
         dev = torch.device("cpu") if device is None else torch.device(device)
         Q, n_r = plan.q_count, plan.frames_of(rank)
-        self.send = torch.empty(2 * Q * n_r, dtype=real, device=dev)
-        # one rank: the send buffer already is the single-source receive buffer
-        self.recv = (self.send if plan.ranks == 1 else
-                     torch.empty(2 * plan.q_of(rank) * plan.frames, dtype=real, device=dev))
+        if exchange not in ("nccl", "p2p"):
+            raise ddm.InputError("exchange must be 'nccl' or 'p2p'")
+        self.exchange_mode = exchange
+        self.symm = None
+        if exchange == "p2p":
+            # receive buffers in symmetric memory: every rank maps every peer's buffer, the
+            # column pass stores into them directly (equal sizes on all ranks)
+            import torch.distributed._symmetric_memory as symm
+            import torch.distributed as dist
+            q_max = max(plan.q_of(r) for r in range(plan.ranks))
+            self.recv = symm.empty(2 * q_max * plan.frames, dtype=real, device=dev)
+            self.symm = symm.rendezvous(self.recv, group if group is not None else dist.group.WORLD)
+            csize = 8 if precision == "f32" else 16
+            ptrs = list(self.symm.buffer_ptrs)
+            # this rank's segment in rank d's buffer: [source][Q_d][n_s], sources before it
+            self.dest = [int(ptrs[d]) + plan.q_of(d) * plan.frame_begin[rank] * csize
+                         for d in range(plan.ranks)]
+            self.send = None
+        else:
+            self.send = torch.empty(2 * Q * n_r, dtype=real, device=dev)
+            # one rank: the send buffer already is the single-source receive buffer
+            self.recv = (self.send if plan.ranks == 1 else
+                         torch.empty(2 * plan.q_of(rank) * plan.frames, dtype=real, device=dev))
         self.out = torch.empty(self.n_lags * max(plan.q_of(rank), 1),
                                dtype=torch.float64 if out_f64 else torch.float32, device=dev)
         self.send_splits = [2 * c for c in plan.send_counts(rank)]
         self.recv_splits = [2 * c for c in plan.recv_counts(rank)]
         self.seg_frames = [plan.frames_of(s) for s in range(plan.ranks)]
 
+    def spatial(self, frames_local) -> None:
+        """Step 1 (with the stores of the fused corner turn in p2p mode)."""
+        n_r = self.plan.frames_of(self.rank)
+        if self.symm is not None:
+            self.symm.barrier(channel=0)   # every peer has consumed its previous receive buffer
+            self.ops.spatial_p2p(frames_local, n_r, self.plan.q_begin, self.dest)
+        else:
+            self.ops.spatial(frames_local, n_r, self.send)
+
     def exchange(self) -> None:
-        """The corner turn: every rank's [Q_d][n_r] block to rank d."""
+        """The corner turn: every rank's [Q_d][n_r] block to rank d (p2p: the blocks are
+        already in place; wait until every rank's stores have landed)."""
+        if self.symm is not None:
+            self.symm.barrier(channel=1)
+            return
         if self.plan.ranks == 1:
             return
         import torch.distributed as dist
@@ -150,7 +196,7 @@ class ShardedRun:
     def step(self, frames_local):
         """Whole sharded pass for this rank; returns the rank's lag-major partial
         [n_lags][Q_r] (a view of `self.out`)."""
-        self.ops.spatial(frames_local, self.plan.frames_of(self.rank), self.send)
+        self.spatial(frames_local)
         self.exchange()
         q_r = self.plan.q_of(self.rank)
         if q_r > 0:

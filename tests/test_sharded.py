@@ -135,9 +135,13 @@ def test_gloo_sharded_matches_single_process(tmp_path, world, W, H, N, precision
 
 # --------------------------------------------------------------------------- GPU
 
-def _virtual_ranks(stack, G, precision="f32", lags=None, out_f64=True):
+def _virtual_ranks(stack, G, precision="f32", lags=None, out_f64=True, exchange="copy"):
     """The sharded pass with G virtual ranks on cuda:0: per-rank spatial shards, the
-    all-to-all as block copies, per-rank temporal over the segments; returns the map."""
+    all-to-all as block copies ("copy") or the fused column-pass stores into every rank's
+    receive buffer ("p2p", the NVLink path with local pointers), per-rank temporal over the
+    segments; returns the map."""
+    if exchange == "p2p":
+        return _virtual_ranks_p2p(stack, G, lags, out_f64)
     import torch
     n, H, W = stack.shape
     Q = H * (W // 2 + 1)
@@ -164,6 +168,57 @@ def _virtual_ranks(stack, G, precision="f32", lags=None, out_f64=True):
         parts.append(out.view(n_lags, q_d).cpu().numpy())
     torch.cuda.synchronize()
     return sharded.assemble(plan, parts).reshape(n_lags, H, W // 2 + 1)
+
+
+def _virtual_ranks_p2p(stack, G, lags=None, out_f64=True):
+    import torch
+    n, H, W = stack.shape
+    Q = H * (W // 2 + 1)
+    plan = sharded.plan_shards(Q, n, G)
+    ops = sharded.DeviceOps(W, H, "f32", device=0)
+    frames = torch.from_numpy(stack.view(np.int16)).cuda()
+    q_max = max(plan.q_of(d) for d in range(G))
+    recvs = [torch.full((2 * q_max * n,), float("nan"), dtype=torch.float32, device="cuda")
+             for _ in range(G)]
+    for r in range(G):
+        dest = [recvs[d].data_ptr() + plan.q_of(d) * plan.frame_begin[r] * 8 for d in range(G)]
+        ops.spatial_p2p(frames[plan.frame_begin[r]: plan.frame_begin[r + 1]], plan.frames_of(r),
+                        plan.q_begin, dest)
+    parts = []
+    n_lags = n if lags is None else len(lags)
+    for d in range(G):
+        q_d = plan.q_of(d)
+        out = torch.empty(n_lags * q_d, dtype=torch.float64 if out_f64 else torch.float32, device="cuda")
+        ops.temporal(recvs[d], q_d, [plan.frames_of(s) for s in range(G)], out, q_d, lags=lags,
+                     out_f64=out_f64)
+        parts.append(out.view(n_lags, q_d).cpu().numpy())
+    torch.cuda.synchronize()
+    return sharded.assemble(plan, parts).reshape(n_lags, H, W // 2 + 1)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("G", [2, 8])
+def test_gpu_fused_p2p_corner_turn(G):
+    """The fused corner turn (column pass storing into the owners' receive buffers) with G
+    virtual ranks: bitwise equal to the unsharded run on the C2 geometry."""
+    st = ddm.generate(512, 512, 1024, particles=100, diffusion=0.5, seed=7)
+    got = _virtual_ranks(st, G, exchange="p2p")
+    ref = ddm.run(st, ddm.RunConfig(precision="f32", memory_bytes=1 << 40)).values
+    np.testing.assert_array_equal(got, ref)
+
+
+@pytest.mark.gpu
+def test_gpu_fused_p2p_small_and_errors():
+    st = O.random_stack(64, 32, 96, seed=3)
+    got = _virtual_ranks(st, 3, exchange="p2p")
+    assert O.relative_l2(got, O.run_with_ft(st, "f32")) <= 1e-4
+    # non power-of-two frames have no register-resident column pass: refused, not faked
+    import torch
+    ops = sharded.DeviceOps(30, 20, "f32", device=0)
+    fr = torch.zeros(30 * 20 * 4, dtype=torch.int16, device="cuda")
+    buf = torch.zeros(2 * 20 * 16 * 4, dtype=torch.float32, device="cuda")
+    with pytest.raises(ddm.InputError):
+        ops.spatial_p2p(fr, 4, [0, 20 * 16], [buf.data_ptr()])
 
 
 @pytest.mark.gpu
