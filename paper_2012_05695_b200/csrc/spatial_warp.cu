@@ -157,13 +157,19 @@ cols2_kernel(const cpx<S>* __restrict__ mid, int Wh, int N, int frame0, int nfra
         constexpr int RS = kThreads / F;
         const int f = threadIdx.x % F, rb = threadIdx.x / F;
         if (f < nf) {
+            const int64_t kstep = (int64_t)RS * Wh;
+            int64_t k = (int64_t)rb * Wh + c;
             int d = 0;
+            int64_t k_end = -1;   // owner slice [.., k_end) of the current destination
+            cpx<S>* dst = nullptr;
 #pragma unroll 4
-            for (int j = 0; j < HL / RS; ++j) {
-                const int64_t k = (int64_t)(rb + RS * j) * Wh + c;
-                while (d + 1 < peers.ranks && k >= peers.q_begin[d + 1]) ++d;
-                cpx<S>* dst = static_cast<cpx<S>*>(peers.base[d]);
-                dst[(k - peers.q_begin[d]) * N + n0 + f] = sm[(rb + RS * j) * SP + f];
+            for (int j = 0; j < HL / RS; ++j, k += kstep, dst += kstep * N) {
+                if (k >= k_end) {  // crossed into the next rank's slice (rare)
+                    while (d + 1 < peers.ranks && k >= peers.q_begin[d + 1]) ++d;
+                    k_end = peers.q_begin[d + 1];
+                    dst = static_cast<cpx<S>*>(peers.base[d]) + (k - peers.q_begin[d]) * N + n0 + f;
+                }
+                *dst = sm[(rb + RS * j) * SP + f];
             }
         }
         return;

@@ -209,7 +209,7 @@ def test_gpu_fused_p2p_corner_turn(G):
 
 @pytest.mark.gpu
 def test_gpu_fused_p2p_small_and_errors():
-    st = O.random_stack(64, 32, 96, seed=3)
+    st = O.random_stack(128, 64, 96, seed=3)
     got = _virtual_ranks(st, 3, exchange="p2p")
     assert O.relative_l2(got, O.run_with_ft(st, "f32")) <= 1e-4
     # non power-of-two frames have no register-resident column pass: refused, not faked
