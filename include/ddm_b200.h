@@ -169,6 +169,24 @@ int ddm_b200_azimuthal(const double* values, int64_t n_lags, int width, int heig
                        int has_q_max, double q_max, int device, double* means,
                        int64_t* counts, int64_t capacity, int64_t* bin_count);
 
+/* ddm::run (WITH_FT) followed by ddm::azimuthal_average (analysis.cpp:61-97), the pair
+   `ddm analyze` calls (tools/ddm_cli.cpp:218-225), in one device pass.  Where the register
+   engines apply (f32, N2 = 2048, power-of-two frames) the ring sums are fused into the
+   temporal kernel and no map is materialised (*fused = 1); otherwise the map goes through HBM
+   and the ring reduction.  means: [n_lags][capacity] f64 (bins beyond bin_count zero);
+   counts (optional, host): per-bin wave-vector counts; d_means = NULL queries bin_count. */
+int ddm_b200_run_azimuthal_device(const void* d_frames, int pixel_bytes, int width, int height,
+                                  int frames, int precision, const int64_t* lags, int64_t n_lags,
+                                  int has_q_max, double q_max, double* d_means, int64_t capacity,
+                                  int64_t* counts, int64_t* bin_count, int device, void* stream,
+                                  double* spatial_ms, double* temporal_ms, int* fused);
+/* The same over host u16 frames and a reference RunConfig; means on the host (NULL = size
+   query); out_lags receives the resolved lag list. */
+int ddm_b200_run_azimuthal_u16(const uint16_t* pixels, int width, int height, int frames,
+                               const ddm_b200_run_config* config, double* means, int64_t capacity,
+                               int64_t* counts, int64_t* bin_count, int64_t* out_lags,
+                               int64_t* out_n_lags);
+
 /* ddm::generate (proj/core/src/synth.cpp:98-132), bit-identical u16 frames. */
 int ddm_b200_generate(int64_t particles, double diffusion, double psf_sigma, double amplitude,
                       double background, int width, int height, int frames,

@@ -497,6 +497,135 @@ void Engine::temporal_segments(const void* d_recv, int64_t q_count, const std::v
     }
 }
 
+RingPlan make_ring_plan(const std::vector<int64_t>& flat, int W, int H) {
+    RingPlan rp;
+    const int Wh = W / 2 + 1;
+    const size_t q = flat.size();
+    std::vector<int64_t> bin(q);
+    int64_t bmax = 0;
+    for (size_t k = 0; k < q; ++k) {
+        const int row = (int)(flat[k] / Wh), col = (int)(flat[k] % Wh);
+        const int qr = row <= H / 2 ? row : row - H;   // `spectrum.hpp:20-24`
+        bin[k] = std::llround(std::sqrt((double)qr * qr + (double)col * col));
+        bmax = std::max(bmax, bin[k]);
+    }
+    rp.nbins = q ? bmax + 1 : 0;
+    rp.counts.assign((size_t)rp.nbins, 0);
+    for (auto b : bin) ++rp.counts[(size_t)b];
+    rp.bin_off.assign((size_t)rp.nbins + 1, 0);
+    for (int64_t b = 0; b < rp.nbins; ++b) rp.bin_off[(size_t)b + 1] = rp.bin_off[(size_t)b] + rp.counts[(size_t)b];
+    rp.by_bin.resize(q);
+    rp.flat_by_bin.resize(q);
+    std::vector<int64_t> fill(rp.bin_off.begin(), rp.bin_off.end() - 1);
+    for (size_t k = 0; k < q; ++k) {
+        const int64_t at = fill[(size_t)bin[k]]++;
+        rp.by_bin[(size_t)at] = (int64_t)k;
+        rp.flat_by_bin[(size_t)at] = flat[k];
+    }
+    std::vector<int64_t> bins;
+    for (int64_t b = 0; b < rp.nbins; ++b)
+        if (rp.counts[(size_t)b] > 0) bins.push_back(b);
+    std::stable_sort(bins.begin(), bins.end(),
+                     [&](int64_t a, int64_t b) { return rp.counts[(size_t)a] > rp.counts[(size_t)b]; });
+    rp.ring_off.assign(1, 0);
+    for (auto b : bins) {
+        rp.ring_bin.push_back(b);
+        for (int64_t i = rp.bin_off[(size_t)b]; i < rp.bin_off[(size_t)b + 1]; ++i)
+            rp.ring_order.push_back(rp.by_bin[(size_t)i]);
+        rp.ring_off.push_back((int64_t)rp.ring_order.size());
+    }
+    return rp;
+}
+
+bool Engine::run_rings(const RunSpec& sp, const RingPlan& rp, double* d_means, PhaseTimes* times) {
+    check(cudaSetDevice(device_), "cudaSetDevice");
+    const int N = sp.N;
+    const int64_t N2 = pad_len(N);
+    const int sb = sp.f64 ? 8 : 4;
+    const int64_t L = (int64_t)sp.lags.size();
+    const int64_t count = sp.groups.empty() ? 0 : sp.groups.back().second;
+    check(cudaMemsetAsync(d_means, 0, (size_t)(L * rp.nbins) * sizeof(double), stream_), "memset");
+    const bool fused = use_warp_temporal(N, (int)N2, sb) &&
+                       ddmk::spatial_warp_supported(sp.W, sp.H, sp.pixel_bytes, sb) &&
+                       std::getenv("DDM_B200_V1_SPATIAL") == nullptr;
+    auto upload = [&](const char* name, const std::vector<int64_t>& v) {
+        void* d = buffer(name, std::max<size_t>(v.size(), 1) * sizeof(int64_t));
+        check(cudaMemcpyAsync(d, v.data(), v.size() * sizeof(int64_t), cudaMemcpyHostToDevice, stream_),
+              "ring upload");
+        return static_cast<const int64_t*>(d);
+    };
+    if (!fused) {
+        // map through HBM (f64), then the deterministic ring reduction
+        RunSpec m = sp;
+        m.out_f64 = true;
+        m.out_stride = (int64_t)sp.H * (sp.W / 2 + 1);
+        m.partial_mode = false;
+        m.groups = {{0, count}};
+        m.d_out = buffer("ring_map", (size_t)(L * m.out_stride) * sizeof(double));
+        if (!sp.identity)
+            check(cudaMemsetAsync(m.d_out, 0, (size_t)(L * m.out_stride) * sizeof(double), stream_), "memset");
+        run(m, times);
+        const int64_t* d_order = upload("ring_flat", rp.flat_by_bin);
+        const int64_t* d_off = upload("ring_binoff", rp.bin_off);
+        radial_means(static_cast<const double*>(m.d_out), L, m.out_stride, d_order, d_off, rp.nbins,
+                     d_means, stream_);
+        check(cudaStreamSynchronize(stream_), "sync");
+        return false;
+    }
+    // fused: spatial pass into the slot-major spectra, then the ring temporal launch
+    const int* d_lag_index = upload_lags(sp.lags, N);
+    const int Wh = sp.W / 2 + 1;
+    const int64_t plane = (int64_t)sp.H * Wh;
+    const int* d_slot = nullptr;
+    std::vector<int> slot_of;
+    if (!sp.identity) {
+        slot_of.assign((size_t)plane, -1);
+        for (size_t k = 0; k < sp.flat.size(); ++k) slot_of[(size_t)sp.flat[k]] = (int)k;
+        check(cudaMemcpyAsync(slotmap_.ensure((size_t)plane * sizeof(int)), slot_of.data(),
+                              (size_t)plane * sizeof(int), cudaMemcpyHostToDevice, stream_), "slot upload");
+        d_slot = static_cast<const int*>(slotmap_.get());
+    }
+    void* d_spec = spec_.ensure((size_t)count * N * 2 * sb);
+    ddmk::SpatialArgs sa = spatial_args(sp.d_frames, sp.pixel_bytes, sp.W, sp.H, N, sp.f64);
+    sa.spec = d_spec;
+    sa.slot_of_flat = d_slot;
+    sa.layout.T = 1;
+    sa.layout.g_begin = 0;
+    sa.layout.g_count = count;
+    if (times) check(cudaEventRecord(ev_[0], stream_), "cudaEventRecord");
+    spatial_pass(sa, sp.f64, true, times);
+    if (times) check(cudaEventRecord(ev_[1], stream_), "cudaEventRecord");
+    ddmk::TemporalArgs ta;
+    ta.spec = d_spec;
+    ta.N = N;
+    ta.N2 = (int)N2;
+    ta.layout.T = 1;
+    ta.layout.g_begin = 0;
+    ta.layout.g_count = count;
+    ta.lag_index = d_lag_index;
+    ta.out_f64 = 1;
+    ta.ring.nrings = (int64_t)rp.ring_bin.size();
+    ta.ring.order = upload("ring_order", rp.ring_order);
+    ta.ring.ring_off = upload("ring_off", rp.ring_off);
+    ta.ring.ring_bin = upload("ring_bin", rp.ring_bin);
+    ta.ring.means = d_means;
+    ta.ring.nbins = rp.nbins;
+    if (times) check(cudaEventRecord(ev_[2], stream_), "cudaEventRecord");
+    check(ddmk::launch_temporal_warp(ta, num_sms_, stream_), "temporal ring kernel");
+    if (times) {
+        check(cudaEventRecord(ev_[3], stream_), "cudaEventRecord");
+        check(cudaEventSynchronize(ev_[3]), "sync");
+        float a = 0.f, b = 0.f;
+        cudaEventElapsedTime(&a, ev_[0], ev_[1]);
+        cudaEventElapsedTime(&b, ev_[2], ev_[3]);
+        times->spatial_ms += a;
+        times->temporal_ms += b;
+        times->temporal_launches += 1;
+    }
+    check(cudaStreamSynchronize(stream_), "sync");  // host vectors consumed by async copies
+    return true;
+}
+
 void Engine::spectra(const void* d_frames, int pixel_bytes, int W, int H, int N, bool f64,
                      void* d_out) {
     check(cudaSetDevice(device_), "cudaSetDevice");

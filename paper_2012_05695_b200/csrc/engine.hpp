@@ -71,6 +71,19 @@ struct RunSpec {
     std::function<void(size_t group, const void* d_partial, int64_t g_count)> on_partial;
 };
 
+// Ring geometry of a retained wave-vector set for the azimuthal average
+// (`analysis.cpp:61-97`): bin = llround(|q|) per retained slot.
+struct RingPlan {
+    int64_t nbins = 0;
+    std::vector<int64_t> counts;     // per bin (geometry only)
+    std::vector<int64_t> bin_off;    // CSR by bin, nbins + 1
+    std::vector<int64_t> by_bin;     // retained slots sorted by bin, ascending within a bin
+    std::vector<int64_t> flat_by_bin;// the same as flat plane positions
+    // fused-kernel work order: non-empty bins, largest first
+    std::vector<int64_t> ring_off, ring_bin, ring_order;
+};
+RingPlan make_ring_plan(const std::vector<int64_t>& flat, int W, int H);
+
 class Engine {
 public:
     explicit Engine(int device);
@@ -112,6 +125,13 @@ public:
     void temporal_segments(const void* d_recv, int64_t q_count, const std::vector<int>& seg_frames,
                            bool f64, const std::vector<int64_t>& lags, void* d_out,
                            int64_t out_stride, bool out_f64, PhaseTimes* times = nullptr);
+
+    // WITH_FT + azimuthal average in one pass (single group): d_means [lags][nbins] f64 on
+    // device. Register engines: the ring sums are fused into the temporal kernel and no map
+    // is materialised (returns true); otherwise the map goes through a device f64 buffer and
+    // the ring reduction (returns false).
+    bool run_rings(const RunSpec& spec, const RingPlan& rings, double* d_means,
+                   PhaseTimes* times = nullptr);
 
     // Device staging buffer for frames owned by the engine.
     void* frame_buffer(size_t bytes) { return frames_.ensure(bytes); }

@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <cstring>
 #include <new>
+#include <optional>
 #include <string>
 
 namespace {
@@ -370,6 +371,140 @@ int ddm_b200_temporal_segments_device(const void* d_recv, int64_t q_count, int n
                                       out_f64 != 0, ms ? &t : nullptr);
                 if (ms) *ms = t.temporal_ms;
             });
+            return 0;
+        });
+    });
+}
+
+namespace {
+
+// shared body of the azimuthal entry points: frames already on the device
+void run_azimuthal_on_device(ddm::b200::Engine& eng, const void* d_frames, int pixel_bytes,
+                             int width, int height, int frames, bool f64,
+                             const std::vector<int64_t>& lag_list, int has_q_max, double q_max,
+                             double* d_means, int64_t capacity, int64_t* counts,
+                             int64_t* bin_count, ddm::b200::PhaseTimes* t, int* fused) {
+    const int64_t plane = int64_t(height) * (width / 2 + 1);
+    ddm::b200::RunSpec sp;
+    sp.W = width;
+    sp.H = height;
+    sp.N = frames;
+    sp.f64 = f64;
+    sp.pixel_bytes = pixel_bytes;
+    sp.d_frames = d_frames;
+    sp.lags = lag_list;
+    sp.identity = true;
+    int64_t count = plane;
+    if (has_q_max) {
+        const auto wv = ddm::cutoff_set(width, height, std::optional<double>(q_max));
+        count = wv.count();
+        if (count < 1) throw ddm::InputError("wave-vector cutoff retains nothing");
+        sp.flat.resize(size_t(count));
+        for (int64_t k = 0; k < count; ++k) {
+            sp.flat[size_t(k)] = wv.flat(k);
+            if (sp.flat[size_t(k)] != k) sp.identity = false;
+        }
+    } else {
+        sp.flat.resize(size_t(plane));
+        for (int64_t k = 0; k < plane; ++k) sp.flat[size_t(k)] = k;
+    }
+    sp.groups = {{0, count}};
+    sp.out_stride = plane;
+    const auto rp = ddm::b200::make_ring_plan(sp.flat, width, height);
+    if (bin_count) *bin_count = rp.nbins;
+    if (counts) std::copy(rp.counts.begin(), rp.counts.begin() + std::min(capacity, rp.nbins), counts);
+    if (!d_means) return;  // size query
+    if (capacity < rp.nbins) throw ddm::InputError("means capacity smaller than the bin count");
+    // means are [lags][capacity]: run into [lags][nbins] then widen if the caller's pitch differs
+    double* target = d_means;
+    if (capacity != rp.nbins)
+        target = static_cast<double*>(eng.buffer("ring_means", size_t(lag_list.size() * rp.nbins) * 8));
+    const bool f = eng.run_rings(sp, rp, target, t);
+    if (fused) *fused = f ? 1 : 0;
+    if (target != d_means) {
+        ddm::b200::check(cudaMemsetAsync(d_means, 0, size_t(lag_list.size() * capacity) * 8, eng.stream()), "memset");
+        ddm::b200::check(cudaMemcpy2DAsync(d_means, size_t(capacity) * 8, target, size_t(rp.nbins) * 8,
+                                           size_t(rp.nbins) * 8, lag_list.size(), cudaMemcpyDeviceToDevice,
+                                           eng.stream()), "copy");
+    }
+}
+
+}  // namespace
+
+int ddm_b200_run_azimuthal_device(const void* d_frames, int pixel_bytes, int width, int height,
+                                  int frames, int precision, const int64_t* lags, int64_t n_lags,
+                                  int has_q_max, double q_max, double* d_means, int64_t capacity,
+                                  int64_t* counts, int64_t* bin_count, int device, void* stream,
+                                  double* spatial_ms, double* temporal_ms, int* fused) {
+    return guarded([&] {
+        if (!d_frames) throw ddm::InputError("null device buffer");
+        if (pixel_bytes != 1 && pixel_bytes != 2) throw ddm::InputError("pixel_bytes must be 1 or 2");
+        if (width < 1 || height < 1 || frames < 1) throw ddm::InputError("dimensions must be positive");
+        const bool f64 = precision != 0;
+        if (frames > ddm::b200::max_frames(f64))
+            throw ddm::PlanError("sequence longer than the device temporal engine limit");
+        std::vector<int64_t> lag_list = (lags && n_lags > 0)
+                                            ? ddm::normalize_lags({lags, lags + n_lags}, frames)
+                                            : ddm::all_lags(frames);
+        ddm::detail::guard_device([&] {
+            auto& eng = ddm::b200::Engine::instance(device);
+            std::lock_guard<std::mutex> lock(eng.mutex());
+            on_engine_stream(eng, stream, [&] {
+                ddm::b200::PhaseTimes t;
+                run_azimuthal_on_device(eng, d_frames, pixel_bytes, width, height, frames, f64,
+                                        lag_list, has_q_max, q_max, d_means, capacity, counts,
+                                        bin_count, (spatial_ms || temporal_ms) ? &t : nullptr, fused);
+                if (spatial_ms) *spatial_ms = t.spatial_ms;
+                if (temporal_ms) *temporal_ms = t.temporal_ms;
+            });
+            return 0;
+        });
+    });
+}
+
+int ddm_b200_run_azimuthal_u16(const uint16_t* pixels, int width, int height, int frames,
+                               const ddm_b200_run_config* config, double* means, int64_t capacity,
+                               int64_t* counts, int64_t* bin_count, int64_t* out_lags,
+                               int64_t* out_n_lags) {
+    return guarded([&] {
+        if (!pixels) throw ddm::InputError("null pixel buffer");
+        const ddm::RunConfig cfg = to_config(config);
+        if (cfg.algorithm != ddm::Algorithm::WithFt)
+            throw ddm::InputError("only the with_ft algorithm runs on the device");
+        if (cfg.workers < 1) throw ddm::InputError("workers must be at least 1");
+        if (width < 1 || height < 1 || frames < 1) throw ddm::InputError("dimensions must be positive");
+        const bool f64 = cfg.precision == ddm::Precision::F64;
+        if (frames > ddm::b200::max_frames(f64))
+            throw ddm::PlanError("sequence longer than the device temporal engine limit");
+        std::vector<int64_t> lag_list = cfg.lags.empty() ? ddm::all_lags(frames)
+                                                         : ddm::normalize_lags(cfg.lags, frames);
+        if (out_n_lags) *out_n_lags = int64_t(lag_list.size());
+        if (out_lags) std::copy(lag_list.begin(), lag_list.end(), out_lags);
+        ddm::detail::guard_device([&] {
+            auto& eng = ddm::b200::Engine::instance(cfg.device);
+            std::lock_guard<std::mutex> lock(eng.mutex());
+            const size_t fb = size_t(frames) * size_t(width) * size_t(height) * 2;
+            void* d_frames = eng.frame_buffer(fb);
+            if (!means) {  // size query only
+                run_azimuthal_on_device(eng, d_frames, 2, width, height, frames, f64, lag_list,
+                                        cfg.q_max.has_value(), cfg.q_max.value_or(0.0), nullptr,
+                                        capacity, counts, bin_count, nullptr, nullptr);
+                return 0;
+            }
+            ddm::b200::check(cudaMemcpyAsync(d_frames, pixels, fb, cudaMemcpyHostToDevice, eng.stream()),
+                             "frame upload");
+            int64_t nb = 0;
+            run_azimuthal_on_device(eng, d_frames, 2, width, height, frames, f64, lag_list,
+                                    cfg.q_max.has_value(), cfg.q_max.value_or(0.0), nullptr, 0,
+                                    nullptr, &nb, nullptr, nullptr);
+            if (capacity < nb) throw ddm::InputError("means capacity smaller than the bin count");
+            double* d_means = static_cast<double*>(eng.buffer("ring_means_out", size_t(lag_list.size() * capacity) * 8));
+            run_azimuthal_on_device(eng, d_frames, 2, width, height, frames, f64, lag_list,
+                                    cfg.q_max.has_value(), cfg.q_max.value_or(0.0), d_means, capacity,
+                                    counts, bin_count, nullptr, nullptr);
+            ddm::b200::check(cudaMemcpyAsync(means, d_means, size_t(lag_list.size() * capacity) * 8,
+                                             cudaMemcpyDeviceToHost, eng.stream()), "download");
+            ddm::b200::check(cudaStreamSynchronize(eng.stream()), "sync");
             return 0;
         });
     });

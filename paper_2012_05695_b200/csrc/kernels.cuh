@@ -62,6 +62,19 @@ struct SegTable {
     int64_t base[kMax] = {};           // complex offset of segment s's [q][n[s]] block
 };
 
+// Fused azimuthal (q-ring) average (`analysis.cpp:61-97`) in the warp engine: rings are
+// processed in the order `ring_off` lists them; ring r holds the sequence slots
+// order[ring_off[r] .. ring_off[r+1]) (ascending within the ring) and lands in bin
+// ring_bin[r]. means[li * nbins + bin] = mean over the ring of d(q, lag li); no map is written.
+struct RingArgs {
+    int64_t nrings = 0;                 // 0 = map mode
+    const int64_t* order = nullptr;
+    const int64_t* ring_off = nullptr;  // nrings + 1
+    const int64_t* ring_bin = nullptr;  // nrings
+    double* means = nullptr;            // [n_lags][nbins]
+    int64_t nbins = 0;
+};
+
 struct TemporalArgs {
     const void* spec = nullptr;
     SegTable segs;                     // warp engine only (the generic engine repacks first)
@@ -78,6 +91,7 @@ struct TemporalArgs {
     // f64 [slot][N], and the per-slot mean (complex f64) used for the restore
     double* corr_out = nullptr;
     double* mean_out = nullptr;
+    RingArgs ring;                     // warp engine only
 };
 
 template <typename S>

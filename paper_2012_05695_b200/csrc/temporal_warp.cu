@@ -130,12 +130,14 @@ __device__ __forceinline__ void fft1024(cpx<float> (&v)[32], cpx<float>* scratch
 
 // kDiag: the batched SequenceEngine API's extra outputs (corr, mean); compiled out of the
 // run path so none of its predicated f64 work is issued there.
-template <typename OutT, bool FULL, bool kDiag, int kWarps>
+// kRing: fused azimuthal average (RingArgs) instead of the map.
+template <typename OutT, bool FULL, bool kDiag, bool kRing, int kWarps>
 __global__ void __launch_bounds__(32 * kWarps, 1)
 temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant__ SegTable segs, int N_rt, int64_t nq,
                      const int* __restrict__ lag_index, OutT* __restrict__ out,
                      int64_t out_stride, const int64_t* __restrict__ dest_of_slot,
-                     double* __restrict__ corr_out, double* __restrict__ mean_out) {
+                     double* __restrict__ corr_out, double* __restrict__ mean_out,
+                     const __grid_constant__ RingArgs ring) {
     // FULL: N == L, every bound below folds at compile time
     const int N = FULL ? kL : N_rt;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -143,6 +145,7 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
     cpx<float>* tw_even = reinterpret_cast<cpx<float>*>(ws + kWarps);  // [c][a] W_1024^{a c}
     cpx<float>* tw_odd = tw_even + 32 * 32;                              // [c][a] W_2048^{a (2c+1)}
     float* rcp = reinterpret_cast<float*>(tw_odd + 32 * 32);             // 1 / (N - m)
+    float* acc_base = rcp + kL;                                          // kRing: [warp][kPad]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     WarpSmem& my = ws[warp];
@@ -175,9 +178,8 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
 
     const int64_t ntiles = (nq + kWarps - 1) / kWarps;
     const uint32_t bytes = (uint32_t)N * 8u;
-    auto prefetch = [&](int64_t tile) {
-        const int64_t q = tile * kWarps + warp;
-        if (lane == 0 && tile < ntiles && q < nq) {
+    auto prefetch_q = [&](int64_t q) {   // q < 0: nothing to fetch
+        if (lane == 0 && q >= 0) {
             if (segs.count == 0) {
                 bulk_load(my.stage, spec + q * (int64_t)N, bytes, &my.bar);
             } else {
@@ -190,11 +192,15 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
         }
     };
 
-    uint32_t phase = 0u;
-    prefetch(blockIdx.x);
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    auto tile_q = [&](int64_t tile) -> int64_t {
         const int64_t q = tile * kWarps + warp;
-        const bool live = q < nq;
+        return (tile < ntiles && q < nq) ? q : -1;
+    };
+
+    uint32_t phase = 0u;
+    // One sequence: wait for its copy, transform, call after_reload() once the stage is free
+    // (to start the next copy), emit(m, d(m)) for every m < N.
+    auto process = [&](int64_t q, bool live, auto&& after_reload, auto&& emit) {
         if (live) {
             mbar_wait(&my.bar, phase);
             phase ^= 1u;
@@ -260,7 +266,7 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
         }
         __syncwarp();
         // the stage is free: start the next sequence's copy (it lands during three FFTs)
-        prefetch(tile + gridDim.x);
+        after_reload();
 #pragma unroll
         for (int b = 0; b < 32; ++b)
             my.pw[padded(lane + 32 * b)] = v[b].x * v[b].x + v[b].y * v[b].y;
@@ -322,7 +328,7 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
             const float re2 = (A.x + Bc.x) + (w.x * (A.y + Bc.y) + w.y * (A.x - Bc.x));
             if (m < N) {
                 const float val = fmaf(-re2, inv_n2, sv[d]) * rcp[m];
-                scf[padded(m)] = (m == 0) ? 0.f : val;
+                emit(m, (m == 0) ? 0.f : val);
                 if constexpr (kDiag)
                     if (corr_out && live) corr_out[q * N + m] = 0.5 * (double)re2 / (double)kN2;
             }
@@ -331,6 +337,58 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
             mean_out[2 * q] = (double)mx;
             mean_out[2 * q + 1] = (double)my_;
         }
+    };
+
+    if constexpr (kRing) {
+        // ---- fused azimuthal average: the CTA takes whole rings (deterministic sums: warp w
+        //      owns items w, w + kWarps, ... of a ring; warps are combined in order, in f64)
+        float* acc = acc_base + warp * kPad;
+        auto first_from = [&](int64_t r, int64_t& rr, int64_t& ii) {
+            for (rr = r; rr < ring.nrings; rr += gridDim.x) {
+                ii = ring.ring_off[rr] + warp;
+                if (ii < ring.ring_off[rr + 1]) return;
+            }
+            ii = -1;
+        };
+        int64_t pr, pi;   // the next item this warp fetches
+        first_from(blockIdx.x, pr, pi);
+        prefetch_q(pi >= 0 ? ring.order[pi] : -1);
+        for (int64_t r = blockIdx.x; r < ring.nrings; r += gridDim.x) {
+            const int64_t beg = ring.ring_off[r], end = ring.ring_off[r + 1];
+#pragma unroll
+            for (int d = 0; d < 32; ++d) acc[padded(lane + 32 * d)] = 0.f;
+            for (int64_t i = beg + warp; i < end; i += kWarps) {
+                const int64_t q = ring.order[i];
+                process(q, true,
+                        [&] {
+                            if (i + kWarps < end) pi = i + kWarps;
+                            else first_from(r + gridDim.x, pr, pi);
+                            prefetch_q(pi >= 0 ? ring.order[pi] : -1);
+                        },
+                        [&](int m, float val) { acc[padded(m)] += val; });
+            }
+            __syncthreads();
+            const int64_t bin = ring.ring_bin[r];
+            const double inv_count = 1.0 / (double)(end - beg);
+            for (int m = threadIdx.x; m < N; m += blockDim.x) {
+                const int li = lag_index ? lag_index[m] : m;
+                if (li < 0) continue;
+                double sum = 0.0;
+#pragma unroll
+                for (int w = 0; w < kWarps; ++w) sum += (double)acc_base[w * kPad + padded(m)];
+                ring.means[(int64_t)li * ring.nbins + bin] = sum * inv_count;
+            }
+            __syncthreads();
+        }
+        return;
+    }
+
+    prefetch_q(tile_q(blockIdx.x));
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t q = tile * kWarps + warp;
+        const bool live = q < nq;
+        process(q, live, [&] { prefetch_q(tile_q(tile + gridDim.x)); },
+                [&](int m, float val) { scf[padded(m)] = val; });
 
         // ---- tile store: lag rows of kWarps consecutive wave vectors (32 B runs for f32)
         __syncthreads();
@@ -384,19 +442,22 @@ namespace {
 // 8 warps (wave vectors) per CTA: 255 registers without spills, one CTA per SM
 constexpr int kTW = 8;
 
-template <typename OutT, bool kDiag>
+template <typename OutT, bool kDiag, bool kRing>
 cudaError_t launch_w(const TemporalArgs& a, int num_sms, cudaStream_t stream) {
     constexpr int W = kTW;
-    const size_t smem = sizeof(WarpSmem) * W + 2 * 32 * 32 * sizeof(cpx<float>) + kL * sizeof(float);
-    const int64_t tiles = (a.layout.g_count + W - 1) / W;
-    const int grid = (int)std::min<int64_t>(tiles, (int64_t)num_sms);
+    const size_t smem = sizeof(WarpSmem) * W + 2 * 32 * 32 * sizeof(cpx<float>) + kL * sizeof(float) +
+                        (kRing ? (size_t)W * kPad * sizeof(float) : 0);
+    const int64_t work = kRing ? a.ring.nrings : (a.layout.g_count + W - 1) / W;
+    const int grid = (int)std::min<int64_t>(work, (int64_t)num_sms);
     if (grid == 0) return cudaSuccess;
     const cpx<float>* spec = static_cast<const cpx<float>*>(a.spec);
-    auto k = a.N == kL ? temporal_warp_kernel<OutT, true, kDiag, W> : temporal_warp_kernel<OutT, false, kDiag, W>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    auto k = a.N == kL ? temporal_warp_kernel<OutT, true, kDiag, kRing, W>
+                       : temporal_warp_kernel<OutT, false, kDiag, kRing, W>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
     k<<<grid, 32 * W, smem, stream>>>(spec, a.segs, a.N, a.layout.g_count, a.lag_index,
                                       static_cast<OutT*>(a.out), a.out_stride, a.dest_of_slot,
-                                      a.corr_out, a.mean_out);
+                                      a.corr_out, a.mean_out, a.ring);
     return cudaGetLastError();
 }
 
@@ -420,11 +481,13 @@ bool temporal_warp_segments_ok(const SegTable& segs, int N) {
 cudaError_t launch_temporal_warp(const TemporalArgs& a, int num_sms, cudaStream_t stream) {
     if (reinterpret_cast<uintptr_t>(a.spec) % 16 != 0) return cudaErrorMisalignedAddress;
     if (!temporal_warp_segments_ok(a.segs, a.N)) return cudaErrorInvalidValue;
+    if (a.ring.nrings > 0) return launch_w<float, false, true>(a, num_sms, stream);
     if (a.corr_out || a.mean_out) {
         if (!a.out_f64) return cudaErrorInvalidValue;
-        return launch_w<double, true>(a, num_sms, stream);
+        return launch_w<double, true, false>(a, num_sms, stream);
     }
-    return a.out_f64 ? launch_w<double, false>(a, num_sms, stream) : launch_w<float, false>(a, num_sms, stream);
+    return a.out_f64 ? launch_w<double, false, false>(a, num_sms, stream)
+                     : launch_w<float, false, false>(a, num_sms, stream);
 }
 
 }  // namespace ddmk

@@ -332,6 +332,50 @@ def azimuthal_average(values, width: int, height: int, q_max: Optional[float] = 
     return means[: L * b].reshape(L, b), counts[:b].copy()
 
 
+def run_azimuthal(stack, config: RunConfig):
+    """ddm::run + ddm::azimuthal_average in one device pass (what `ddm analyze` computes,
+    `ddm_cli.cpp:218-225`), ring sums fused into the temporal kernel where the register engines
+    apply. Returns (means [L, bins], counts [bins], lags)."""
+    st = np.ascontiguousarray(np.asarray(stack), dtype=np.uint16)
+    if st.ndim != 3:
+        raise InputError("stack must be [frames, height, width]")
+    n, h, w = st.shape
+    keep: list = []
+    c = _config(config, keep)
+    nb = C.c_int64(0)
+    n_out = len(config.lags) if len(config.lags) else n
+    out_lags = np.zeros(max(n_out, 1), dtype=np.int64)
+    nl = C.c_int64(0)
+    _check(lib().ddm_b200_run_azimuthal_u16(_p(st, C.c_uint16), w, h, n, C.byref(c), None,
+                                            C.c_int64(0), None, C.byref(nb), _p(out_lags, C.c_int64),
+                                            C.byref(nl)))
+    b = nb.value
+    means = np.zeros(max(nl.value, 1) * b)
+    counts = np.zeros(b, dtype=np.int64)
+    _check(lib().ddm_b200_run_azimuthal_u16(_p(st, C.c_uint16), w, h, n, C.byref(c),
+                                            _p(means, C.c_double), C.c_int64(b),
+                                            _p(counts, C.c_int64), C.byref(nb),
+                                            _p(out_lags, C.c_int64), C.byref(nl)))
+    k = nl.value
+    return means[: k * b].reshape(k, b), counts, out_lags[:k].copy()
+
+
+def run_azimuthal_device(frames_ptr: int, pixel_bytes: int, width: int, height: int, frames: int,
+                         means_ptr: int, capacity: int, precision: str = "f32", lags=None,
+                         q_max: Optional[float] = None, device: int = 0, stream: int = 0):
+    """Device-resident run + ring average: means [L][capacity] f64 at means_ptr (HBM).
+    Returns (bin_count, spatial_ms, temporal_ms, fused)."""
+    lag_arr = np.ascontiguousarray(np.asarray(lags if lags is not None else [], dtype=np.int64))
+    nb, sp, tp, fu = C.c_int64(0), C.c_double(0), C.c_double(0), C.c_int(0)
+    _check(lib().ddm_b200_run_azimuthal_device(
+        C.c_void_p(frames_ptr), pixel_bytes, width, height, frames,
+        0 if precision == "f32" else 1, _p(lag_arr, C.c_int64) if len(lag_arr) else None,
+        C.c_int64(len(lag_arr)), 0 if q_max is None else 1,
+        C.c_double(0.0 if q_max is None else q_max), C.c_void_p(means_ptr), C.c_int64(capacity),
+        None, C.byref(nb), device, C.c_void_p(stream), C.byref(sp), C.byref(tp), C.byref(fu)))
+    return nb.value, sp.value, tp.value, bool(fu.value)
+
+
 def generate(width=64, height=64, frames=256, particles=100, diffusion=0.5, psf_sigma=1.0,
              amplitude=1000.0, background=100.0, frame_interval=1.0, seed=0) -> np.ndarray:
     """ddm::generate (`synth.cpp:98-132`), bit-identical frames [N, H, W] uint16."""

@@ -321,3 +321,38 @@ def test_c5_non_power_of_two(ddm):
     ref = O.direct_sequence(np.ascontiguousarray(sp[:, idx].T)).T
     ref[0] = 0.0
     assert O.relative_deviation(vals[:, idx], ref) <= 1e-9
+
+
+# --------------------------------------------------------------------------- fused ring average
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("W,H,N,prec,q_max,lags", [
+    (512, 512, 1024, "f32", None, None),       # C2 geometry: fused into the warp engine
+    (128, 64, 600, "f32", 20.0, [0, 1, 7, 599]),  # fused, cutoff + lag subset, N < L
+    (64, 48, 100, "f64", None, None),          # generic engines: map + ring reduction
+    (500, 500, 1000, "f32", None, [1, 10, 100, 999]),  # non-power-of-two frames (C5)
+])
+def test_run_azimuthal_matches_oracle(ddm, W, H, N, prec, q_max, lags):
+    st = ddm.generate(W, H, N, particles=100, diffusion=0.5, seed=11)
+    cfg = ddm.RunConfig(precision=prec, memory_bytes=1 << 40, q_max=q_max,
+                        lags=lags if lags is not None else [])
+    means, counts, got_lags = ddm.run_azimuthal(st, cfg)
+    ref_map = O.run_with_ft(st, prec, lags=lags, q_max=q_max)
+    ref_means, ref_counts = O.azimuthal_average(ref_map, W, H, q_max)
+    np.testing.assert_array_equal(counts, ref_counts)
+    assert list(got_lags) == O.normalize_lags(lags, N)
+    tol = 1e-4 if prec == "f32" else 1e-10
+    assert O.relative_l2(means, ref_means) <= tol
+    assert np.all(means[got_lags == 0] == 0.0)
+
+
+@pytest.mark.gpu
+def test_run_azimuthal_fused_equals_map_then_average(ddm):
+    """The fused ring sums and the two-step device path (map, then ring reduction) agree."""
+    st = ddm.generate(256, 256, 1024, particles=80, diffusion=0.4, seed=5)
+    cfg = ddm.RunConfig(precision="f32", memory_bytes=1 << 40)
+    fused, counts, _ = ddm.run_azimuthal(st, cfg)
+    arch = ddm.run(st, cfg)
+    two_step, counts2 = ddm.azimuthal_average(arch.values, 256, 256)
+    np.testing.assert_array_equal(counts, counts2)
+    assert O.relative_l2(fused, two_step) <= 1e-6
