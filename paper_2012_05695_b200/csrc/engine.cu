@@ -522,23 +522,47 @@ RingPlan make_ring_plan(const std::vector<int64_t>& flat, int W, int H) {
         rp.by_bin[(size_t)at] = (int64_t)k;
         rp.flat_by_bin[(size_t)at] = flat[k];
     }
-    std::vector<int64_t> bins;
-    for (int64_t b = 0; b < rp.nbins; ++b)
-        if (rp.counts[(size_t)b] > 0) bins.push_back(b);
-    std::stable_sort(bins.begin(), bins.end(),
-                     [&](int64_t a, int64_t b) { return rp.counts[(size_t)a] > rp.counts[(size_t)b]; });
-    rp.ring_off.assign(1, 0);
-    for (auto b : bins) {
+    rp.item_off.assign(1, 0);
+    rp.ring_item_off.assign(1, 0);
+    for (int64_t b = 0; b < rp.nbins; ++b) {
+        const int64_t c = rp.counts[(size_t)b];
+        if (c == 0) continue;
+        for (int64_t i = rp.bin_off[(size_t)b]; i < rp.bin_off[(size_t)b + 1]; i += RingPlan::kItem)
+            rp.item_off.push_back(std::min(i + RingPlan::kItem, rp.bin_off[(size_t)b + 1]));
+        rp.ring_item_off.push_back((int64_t)rp.item_off.size() - 1);
         rp.ring_bin.push_back(b);
-        for (int64_t i = rp.bin_off[(size_t)b]; i < rp.bin_off[(size_t)b + 1]; ++i)
-            rp.ring_order.push_back(rp.by_bin[(size_t)i]);
-        rp.ring_off.push_back((int64_t)rp.ring_order.size());
+        rp.ring_count.push_back(c);
     }
     return rp;
 }
 
+const RingPlan& Engine::ring_plan(const std::vector<int64_t>& flat, int W, int H) {
+    RingCache& c = ring_cache_;
+    if (c.plan && c.W == W && c.H == H && c.flat == flat) return *c.plan;
+    c.own = std::make_unique<RingPlan>(make_ring_plan(flat, W, H));
+    c.plan = c.own.get();
+    c.W = W;
+    c.H = H;
+    c.flat = flat;
+    auto up = [&](const char* name, const std::vector<int64_t>& v) {
+        void* d = buffer(name, std::max<size_t>(v.size(), 1) * sizeof(int64_t));
+        check(cudaMemcpy(d, v.data(), v.size() * sizeof(int64_t), cudaMemcpyHostToDevice), "ring upload");
+        return static_cast<const int64_t*>(d);
+    };
+    c.order = up("ring_order", c.plan->by_bin);
+    c.item_off = up("ring_item_off", c.plan->item_off);
+    c.ring_item_off = up("ring_ring_item_off", c.plan->ring_item_off);
+    c.ring_bin = up("ring_bin", c.plan->ring_bin);
+    c.ring_count = up("ring_count", c.plan->ring_count);
+    c.flat_by_bin = up("ring_flat", c.plan->flat_by_bin);
+    c.bin_off = up("ring_bin_off", c.plan->bin_off);
+    return *c.plan;
+}
+
 bool Engine::run_rings(const RunSpec& sp, const RingPlan& rp, double* d_means, PhaseTimes* times) {
     check(cudaSetDevice(device_), "cudaSetDevice");
+    if (&rp != ring_cache_.plan) throw std::invalid_argument("run_rings: plan must come from ring_plan()");
+    const RingCache& rc = ring_cache_;
     const int N = sp.N;
     const int64_t N2 = pad_len(N);
     const int sb = sp.f64 ? 8 : 4;
@@ -548,12 +572,6 @@ bool Engine::run_rings(const RunSpec& sp, const RingPlan& rp, double* d_means, P
     const bool fused = use_warp_temporal(N, (int)N2, sb) &&
                        ddmk::spatial_warp_supported(sp.W, sp.H, sp.pixel_bytes, sb) &&
                        std::getenv("DDM_B200_V1_SPATIAL") == nullptr;
-    auto upload = [&](const char* name, const std::vector<int64_t>& v) {
-        void* d = buffer(name, std::max<size_t>(v.size(), 1) * sizeof(int64_t));
-        check(cudaMemcpyAsync(d, v.data(), v.size() * sizeof(int64_t), cudaMemcpyHostToDevice, stream_),
-              "ring upload");
-        return static_cast<const int64_t*>(d);
-    };
     if (!fused) {
         // map through HBM (f64), then the deterministic ring reduction
         RunSpec m = sp;
@@ -565,10 +583,8 @@ bool Engine::run_rings(const RunSpec& sp, const RingPlan& rp, double* d_means, P
         if (!sp.identity)
             check(cudaMemsetAsync(m.d_out, 0, (size_t)(L * m.out_stride) * sizeof(double), stream_), "memset");
         run(m, times);
-        const int64_t* d_order = upload("ring_flat", rp.flat_by_bin);
-        const int64_t* d_off = upload("ring_binoff", rp.bin_off);
-        radial_means(static_cast<const double*>(m.d_out), L, m.out_stride, d_order, d_off, rp.nbins,
-                     d_means, stream_);
+        radial_means(static_cast<const double*>(m.d_out), L, m.out_stride, rc.flat_by_bin, rc.bin_off,
+                     rp.nbins, d_means, stream_);
         check(cudaStreamSynchronize(stream_), "sync");
         return false;
     }
@@ -595,6 +611,7 @@ bool Engine::run_rings(const RunSpec& sp, const RingPlan& rp, double* d_means, P
     if (times) check(cudaEventRecord(ev_[0], stream_), "cudaEventRecord");
     spatial_pass(sa, sp.f64, true, times);
     if (times) check(cudaEventRecord(ev_[1], stream_), "cudaEventRecord");
+    const int64_t nitems = (int64_t)rp.item_off.size() - 1;
     ddmk::TemporalArgs ta;
     ta.spec = d_spec;
     ta.N = N;
@@ -604,14 +621,15 @@ bool Engine::run_rings(const RunSpec& sp, const RingPlan& rp, double* d_means, P
     ta.layout.g_count = count;
     ta.lag_index = d_lag_index;
     ta.out_f64 = 1;
-    ta.ring.nrings = (int64_t)rp.ring_bin.size();
-    ta.ring.order = upload("ring_order", rp.ring_order);
-    ta.ring.ring_off = upload("ring_off", rp.ring_off);
-    ta.ring.ring_bin = upload("ring_bin", rp.ring_bin);
-    ta.ring.means = d_means;
-    ta.ring.nbins = rp.nbins;
+    ta.ring.nitems = nitems;
+    ta.ring.order = rc.order;
+    ta.ring.item_off = rc.item_off;
+    ta.ring.partial = static_cast<double*>(buffer("ring_partial", (size_t)(nitems * N) * sizeof(double)));
     if (times) check(cudaEventRecord(ev_[2], stream_), "cudaEventRecord");
     check(ddmk::launch_temporal_warp(ta, num_sms_, stream_), "temporal ring kernel");
+    check(ddmk::launch_ring_means(ta.ring.partial, N, d_lag_index, rc.ring_item_off, rc.ring_bin,
+                                  rc.ring_count, (int64_t)rp.ring_bin.size(), d_means, rp.nbins,
+                                  stream_), "ring means kernel");
     if (times) {
         check(cudaEventRecord(ev_[3], stream_), "cudaEventRecord");
         check(cudaEventSynchronize(ev_[3]), "sync");
@@ -620,9 +638,9 @@ bool Engine::run_rings(const RunSpec& sp, const RingPlan& rp, double* d_means, P
         cudaEventElapsedTime(&b, ev_[2], ev_[3]);
         times->spatial_ms += a;
         times->temporal_ms += b;
-        times->temporal_launches += 1;
+        times->temporal_launches += 2;
     }
-    check(cudaStreamSynchronize(stream_), "sync");  // host vectors consumed by async copies
+    if (!sp.identity) check(cudaStreamSynchronize(stream_), "sync");  // slot_of is host-side
     return true;
 }
 

@@ -75,12 +75,15 @@ struct RunSpec {
 // (`analysis.cpp:61-97`): bin = llround(|q|) per retained slot.
 struct RingPlan {
     int64_t nbins = 0;
-    std::vector<int64_t> counts;     // per bin (geometry only)
-    std::vector<int64_t> bin_off;    // CSR by bin, nbins + 1
-    std::vector<int64_t> by_bin;     // retained slots sorted by bin, ascending within a bin
-    std::vector<int64_t> flat_by_bin;// the same as flat plane positions
-    // fused-kernel work order: non-empty bins, largest first
-    std::vector<int64_t> ring_off, ring_bin, ring_order;
+    std::vector<int64_t> counts;       // per bin (geometry only)
+    std::vector<int64_t> bin_off;      // CSR by bin, nbins + 1
+    std::vector<int64_t> by_bin;       // retained slots sorted by bin, ascending within a bin
+    std::vector<int64_t> flat_by_bin;  // the same as flat plane positions
+    // fused-kernel work items (ring pieces of <= kItem slots, in by_bin order) and rings
+    std::vector<int64_t> item_off;       // nitems + 1, offsets into by_bin
+    std::vector<int64_t> ring_item_off;  // nrings + 1, offsets into the items
+    std::vector<int64_t> ring_bin, ring_count;
+    static constexpr int64_t kItem = 64;
 };
 RingPlan make_ring_plan(const std::vector<int64_t>& flat, int W, int H);
 
@@ -131,7 +134,7 @@ public:
     // is materialised (returns true); otherwise the map goes through a device f64 buffer and
     // the ring reduction (returns false).
     bool run_rings(const RunSpec& spec, const RingPlan& rings, double* d_means,
-                   PhaseTimes* times = nullptr);
+                   PhaseTimes* times = nullptr);  // rings: from ring_plan()
 
     // Device staging buffer for frames owned by the engine.
     void* frame_buffer(size_t bytes) { return frames_.ensure(bytes); }
@@ -172,6 +175,20 @@ private:
     std::vector<cudaEvent_t> chunk_events_;    // row/column pass ordering across streams
     cudaStream_t cols_stream_ = nullptr;       // column passes (overlapped spatial step)
     std::mutex mu_;
+    // last ring plan and its device copy (geometry only, reused across runs)
+    struct RingCache {
+        int W = 0, H = 0;
+        std::vector<int64_t> flat;
+        const RingPlan* plan = nullptr;
+        std::unique_ptr<RingPlan> own;
+        const int64_t *order = nullptr, *item_off = nullptr, *ring_item_off = nullptr,
+                      *ring_bin = nullptr, *ring_count = nullptr, *flat_by_bin = nullptr,
+                      *bin_off = nullptr;
+    } ring_cache_;
+
+public:
+    // ring plan of (flat, W, H), built once and cached with its device arrays
+    const RingPlan& ring_plan(const std::vector<int64_t>& flat, int W, int H);
 };
 
 // Hardware limits of the one-CTA temporal kernel (longest supported sequence).

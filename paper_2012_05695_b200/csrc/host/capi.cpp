@@ -410,7 +410,7 @@ void run_azimuthal_on_device(ddm::b200::Engine& eng, const void* d_frames, int p
     }
     sp.groups = {{0, count}};
     sp.out_stride = plane;
-    const auto rp = ddm::b200::make_ring_plan(sp.flat, width, height);
+    const auto& rp = eng.ring_plan(sp.flat, width, height);
     if (bin_count) *bin_count = rp.nbins;
     if (counts) std::copy(rp.counts.begin(), rp.counts.begin() + std::min(capacity, rp.nbins), counts);
     if (!d_means) return;  // size query

@@ -62,17 +62,17 @@ struct SegTable {
     int64_t base[kMax] = {};           // complex offset of segment s's [q][n[s]] block
 };
 
-// Fused azimuthal (q-ring) average (`analysis.cpp:61-97`) in the warp engine: rings are
-// processed in the order `ring_off` lists them; ring r holds the sequence slots
-// order[ring_off[r] .. ring_off[r+1]) (ascending within the ring) and lands in bin
-// ring_bin[r]. means[li * nbins + bin] = mean over the ring of d(q, lag li); no map is written.
+// Fused azimuthal (q-ring) average (`analysis.cpp:61-97`) in the warp engine. The retained
+// sequence slots, sorted by ring (bin) and ascending within a ring, are `order`; they are cut
+// into work items of at most a few dozen slots that never straddle a ring:
+// item i = order[item_off[i] .. item_off[i+1]). The temporal kernel writes, per item, the f64
+// sum over its slots of d(q, m) for every m (partial[i][m]); ring_means_kernel then adds the
+// items of each ring in order (deterministic) into means[li * nbins + bin] / count.
 struct RingArgs {
-    int64_t nrings = 0;                 // 0 = map mode
+    int64_t nitems = 0;                 // 0 = map mode
     const int64_t* order = nullptr;
-    const int64_t* ring_off = nullptr;  // nrings + 1
-    const int64_t* ring_bin = nullptr;  // nrings
-    double* means = nullptr;            // [n_lags][nbins]
-    int64_t nbins = 0;
+    const int64_t* item_off = nullptr;  // nitems + 1
+    double* partial = nullptr;          // [nitems][N]
 };
 
 struct TemporalArgs {
@@ -99,6 +99,13 @@ cudaError_t launch_spatial(const SpatialArgs& a, cudaStream_t stream);
 
 template <typename S>
 cudaError_t launch_temporal(const TemporalArgs& a, cudaStream_t stream);
+
+// Ring means from the per-item partial sums: ring r = items [ring_item_off[r],
+// ring_item_off[r+1]) with ring_count[r] slots, landing in bin ring_bin[r].
+cudaError_t launch_ring_means(const double* partial, int N, const int* lag_index,
+                              const int64_t* ring_item_off, const int64_t* ring_bin,
+                              const int64_t* ring_count, int64_t nrings, double* means,
+                              int64_t nbins, cudaStream_t stream);
 
 // Segmented sequences (SegTable over q_count sequences) -> the engine's tile-major layout T.
 template <typename S>

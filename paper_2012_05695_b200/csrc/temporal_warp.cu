@@ -340,43 +340,37 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
     };
 
     if constexpr (kRing) {
-        // ---- fused azimuthal average: the CTA takes whole rings (deterministic sums: warp w
-        //      owns items w, w + kWarps, ... of a ring; warps are combined in order, in f64)
+        // ---- fused azimuthal average: work items are ring pieces; warp w owns slots
+        //      w, w + kWarps, ... of an item, warps are combined in order in f64
         float* acc = acc_base + warp * kPad;
-        auto first_from = [&](int64_t r, int64_t& rr, int64_t& ii) {
-            for (rr = r; rr < ring.nrings; rr += gridDim.x) {
-                ii = ring.ring_off[rr] + warp;
-                if (ii < ring.ring_off[rr + 1]) return;
+        auto first_from = [&](int64_t it) -> int64_t {   // this warp's first slot at item >= it
+            for (; it < ring.nitems; it += gridDim.x) {
+                const int64_t i = ring.item_off[it] + warp;
+                if (i < ring.item_off[it + 1]) return i;
             }
-            ii = -1;
+            return -1;
         };
-        int64_t pr, pi;   // the next item this warp fetches
-        first_from(blockIdx.x, pr, pi);
+        int64_t pi = first_from(blockIdx.x);   // the next slot this warp fetches
         prefetch_q(pi >= 0 ? ring.order[pi] : -1);
-        for (int64_t r = blockIdx.x; r < ring.nrings; r += gridDim.x) {
-            const int64_t beg = ring.ring_off[r], end = ring.ring_off[r + 1];
+        for (int64_t it = blockIdx.x; it < ring.nitems; it += gridDim.x) {
+            const int64_t beg = ring.item_off[it], end = ring.item_off[it + 1];
 #pragma unroll
             for (int d = 0; d < 32; ++d) acc[padded(lane + 32 * d)] = 0.f;
             for (int64_t i = beg + warp; i < end; i += kWarps) {
-                const int64_t q = ring.order[i];
-                process(q, true,
+                process(ring.order[i], true,
                         [&] {
-                            if (i + kWarps < end) pi = i + kWarps;
-                            else first_from(r + gridDim.x, pr, pi);
+                            pi = (i + kWarps < end) ? i + kWarps : first_from(it + gridDim.x);
                             prefetch_q(pi >= 0 ? ring.order[pi] : -1);
                         },
                         [&](int m, float val) { acc[padded(m)] += val; });
             }
             __syncthreads();
-            const int64_t bin = ring.ring_bin[r];
-            const double inv_count = 1.0 / (double)(end - beg);
+            double* dst = ring.partial + it * (int64_t)N;
             for (int m = threadIdx.x; m < N; m += blockDim.x) {
-                const int li = lag_index ? lag_index[m] : m;
-                if (li < 0) continue;
                 double sum = 0.0;
 #pragma unroll
                 for (int w = 0; w < kWarps; ++w) sum += (double)acc_base[w * kPad + padded(m)];
-                ring.means[(int64_t)li * ring.nbins + bin] = sum * inv_count;
+                dst[m] = sum;
             }
             __syncthreads();
         }
@@ -447,7 +441,7 @@ cudaError_t launch_w(const TemporalArgs& a, int num_sms, cudaStream_t stream) {
     constexpr int W = kTW;
     const size_t smem = sizeof(WarpSmem) * W + 2 * 32 * 32 * sizeof(cpx<float>) + kL * sizeof(float) +
                         (kRing ? (size_t)W * kPad * sizeof(float) : 0);
-    const int64_t work = kRing ? a.ring.nrings : (a.layout.g_count + W - 1) / W;
+    const int64_t work = kRing ? a.ring.nitems : (a.layout.g_count + W - 1) / W;
     const int grid = (int)std::min<int64_t>(work, (int64_t)num_sms);
     if (grid == 0) return cudaSuccess;
     const cpx<float>* spec = static_cast<const cpx<float>*>(a.spec);
@@ -481,13 +475,49 @@ bool temporal_warp_segments_ok(const SegTable& segs, int N) {
 cudaError_t launch_temporal_warp(const TemporalArgs& a, int num_sms, cudaStream_t stream) {
     if (reinterpret_cast<uintptr_t>(a.spec) % 16 != 0) return cudaErrorMisalignedAddress;
     if (!temporal_warp_segments_ok(a.segs, a.N)) return cudaErrorInvalidValue;
-    if (a.ring.nrings > 0) return launch_w<float, false, true>(a, num_sms, stream);
+    if (a.ring.nitems > 0) return launch_w<float, false, true>(a, num_sms, stream);
     if (a.corr_out || a.mean_out) {
         if (!a.out_f64) return cudaErrorInvalidValue;
         return launch_w<double, true, false>(a, num_sms, stream);
     }
     return a.out_f64 ? launch_w<double, false, false>(a, num_sms, stream)
                      : launch_w<float, false, false>(a, num_sms, stream);
+}
+
+namespace {
+
+// one thread per (lag, ring): items of the ring added in order
+__global__ void ring_means_kernel(const double* __restrict__ partial, int N,
+                                  const int* __restrict__ lag_index,
+                                  const int64_t* __restrict__ ring_item_off,
+                                  const int64_t* __restrict__ ring_bin,
+                                  const int64_t* __restrict__ ring_count, int64_t nrings,
+                                  double* __restrict__ means, int64_t nbins) {
+    const int64_t total = nrings * (int64_t)N;
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total;
+         x += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = x / N;
+        const int m = (int)(x - r * N);
+        const int li = lag_index ? lag_index[m] : m;
+        if (li < 0) continue;
+        double sum = 0.0;
+        for (int64_t it = ring_item_off[r]; it < ring_item_off[r + 1]; ++it) sum += partial[it * N + m];
+        means[(int64_t)li * nbins + ring_bin[r]] = (m == 0) ? 0.0 : sum / (double)ring_count[r];
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_ring_means(const double* partial, int N, const int* lag_index,
+                              const int64_t* ring_item_off, const int64_t* ring_bin,
+                              const int64_t* ring_count, int64_t nrings, double* means,
+                              int64_t nbins, cudaStream_t stream) {
+    const int64_t total = nrings * (int64_t)N;
+    const int blocks = (int)std::min<int64_t>(148 * 8, (total + 255) / 256);
+    if (blocks == 0) return cudaSuccess;
+    ring_means_kernel<<<blocks, 256, 0, stream>>>(partial, N, lag_index, ring_item_off, ring_bin,
+                                                  ring_count, nrings, means, nbins);
+    return cudaGetLastError();
 }
 
 }  // namespace ddmk
