@@ -47,6 +47,11 @@ bool use_warp_temporal(int N, int N2, int sb) {
     return !v1 && ddmk::temporal_warp_supported(N, N2, sb);
 }
 
+bool use_long_temporal(int N, int N2, int sb) {
+    static const bool v1 = std::getenv("DDM_B200_V1") != nullptr;
+    return !v1 && ddmk::temporal_long_supported(N, N2, sb);
+}
+
 int64_t pad_len(int64_t n) {
     int64_t n2 = 1;
     while (n2 < n) n2 <<= 1;
@@ -287,7 +292,8 @@ uint64_t Engine::run(const RunSpec& sp, PhaseTimes* times) {
     const int sb = sp.f64 ? 8 : 4;
     const size_t cs = 2 * (size_t)sb;
     const bool warp_t = use_warp_temporal(N, (int)N2, sb);
-    const int T = warp_t ? 1 : ddmk::temporal_tile(N, (int)N2, sb);
+    const bool long_t = !warp_t && use_long_temporal(N, (int)N2, sb);
+    const int T = (warp_t || long_t) ? 1 : ddmk::temporal_tile(N, (int)N2, sb);
     if (T == 0)
         throw std::length_error("sequence of " + std::to_string(N) +
                                 " frames exceeds the single-CTA temporal engine (max " +
@@ -312,7 +318,7 @@ uint64_t Engine::run(const RunSpec& sp, PhaseTimes* times) {
     for (auto& g : sp.groups) gmax = std::max(gmax, g.second - g.first);
     const int64_t tiles_max = (gmax + T - 1) / T;
     void* d_spec = spec_.ensure((size_t)tiles_max * N * T * cs);
-    const bool warp_s = warp_t && ddmk::spatial_warp_supported(W, H, sp.pixel_bytes, sb) &&
+    const bool warp_s = (warp_t || long_t) && ddmk::spatial_warp_supported(W, H, sp.pixel_bytes, sb) &&
                         std::getenv("DDM_B200_V1_SPATIAL") == nullptr;
     ddmk::SpatialArgs sa = spatial_args(sp.d_frames, sp.pixel_bytes, W, H, N, sp.f64);
     sa.spec = d_spec;
@@ -380,10 +386,18 @@ uint64_t Engine::run(const RunSpec& sp, PhaseTimes* times) {
             ta.dest_of_slot = static_cast<const int64_t*>(dest_.get());
         }
         mark();
-        check(warp_t ? ddmk::launch_temporal_warp(ta, num_sms_, stream_)
-                     : sp.f64 ? ddmk::launch_temporal<double>(ta, stream_)
-                              : ddmk::launch_temporal<float>(ta, stream_), "temporal kernel");
-        if (times) times->temporal_launches += 1;
+        if (long_t) {
+            void* out_q = buffer("long_out_q", (size_t)std::min<int64_t>(gc, ddmk::temporal_long_chunk(N)) *
+                                                   N * sizeof(float));
+            check(ddmk::launch_temporal_long(ta, num_sms_, out_q, stream_), "temporal kernel");
+            if (times) times->temporal_launches += 2 * (int)((gc + ddmk::temporal_long_chunk(N) - 1) /
+                                                             ddmk::temporal_long_chunk(N));
+        } else {
+            check(warp_t ? ddmk::launch_temporal_warp(ta, num_sms_, stream_)
+                         : sp.f64 ? ddmk::launch_temporal<double>(ta, stream_)
+                                  : ddmk::launch_temporal<float>(ta, stream_), "temporal kernel");
+            if (times) times->temporal_launches += 1;
+        }
         mark();
         if (sp.partial_mode && sp.on_partial) sp.on_partial(gi, ta.out, gc);
         // the host-side slot map / dest vectors must outlive the async copies
@@ -453,8 +467,10 @@ void Engine::temporal_segments(const void* d_recv, int64_t q_count, const std::v
     }
     const int64_t N2 = pad_len(N);
     const int sb = f64 ? 8 : 4;
-    const bool warp_t = use_warp_temporal(N, (int)N2, sb) && ddmk::temporal_warp_segments_ok(segs, N);
-    const int T = warp_t ? 1 : ddmk::temporal_tile(N, (int)N2, sb);
+    const bool seg_ok = ddmk::temporal_warp_segments_ok(segs, N);
+    const bool warp_t = use_warp_temporal(N, (int)N2, sb) && seg_ok;
+    const bool long_t = !warp_t && use_long_temporal(N, (int)N2, sb) && seg_ok;
+    const int T = (warp_t || long_t) ? 1 : ddmk::temporal_tile(N, (int)N2, sb);
     if (T == 0)
         throw std::length_error("sequence of " + std::to_string(N) +
                                 " frames exceeds the single-CTA temporal engine");
@@ -471,10 +487,16 @@ void Engine::temporal_segments(const void* d_recv, int64_t q_count, const std::v
     ta.out_f64 = out_f64 ? 1 : 0;
     ta.out_stride = out_stride;
     if (times) check(cudaEventRecord(ev_[2], stream_), "cudaEventRecord");
-    if (warp_t) {
+    if (warp_t || long_t) {
         ta.spec = d_recv;
         ta.segs = segs;
-        check(ddmk::launch_temporal_warp(ta, num_sms_, stream_), "temporal kernel");
+        if (warp_t) {
+            check(ddmk::launch_temporal_warp(ta, num_sms_, stream_), "temporal kernel");
+        } else {
+            void* out_q = buffer("long_out_q", (size_t)std::min<int64_t>(q_count, ddmk::temporal_long_chunk(N)) *
+                                                   N * sizeof(float));
+            check(ddmk::launch_temporal_long(ta, num_sms_, out_q, stream_), "temporal kernel");
+        }
     } else {
         // generic engine: gather the segments into its tile-major layout first
         const int64_t tiles = (q_count + T - 1) / T;
@@ -569,9 +591,11 @@ bool Engine::run_rings(const RunSpec& sp, const RingPlan& rp, double* d_means, P
     const int64_t L = (int64_t)sp.lags.size();
     const int64_t count = sp.groups.empty() ? 0 : sp.groups.back().second;
     check(cudaMemsetAsync(d_means, 0, (size_t)(L * rp.nbins) * sizeof(double), stream_), "memset");
-    const bool fused = use_warp_temporal(N, (int)N2, sb) &&
-                       ddmk::spatial_warp_supported(sp.W, sp.H, sp.pixel_bytes, sb) &&
-                       std::getenv("DDM_B200_V1_SPATIAL") == nullptr;
+    const bool warp_t = use_warp_temporal(N, (int)N2, sb);
+    const bool long_t = !warp_t && use_long_temporal(N, (int)N2, sb);
+    const bool fused = warp_t || long_t;
+    const bool warp_s = fused && ddmk::spatial_warp_supported(sp.W, sp.H, sp.pixel_bytes, sb) &&
+                        std::getenv("DDM_B200_V1_SPATIAL") == nullptr;
     if (!fused) {
         // map through HBM (f64), then the deterministic ring reduction
         RunSpec m = sp;
@@ -609,7 +633,7 @@ bool Engine::run_rings(const RunSpec& sp, const RingPlan& rp, double* d_means, P
     sa.layout.g_begin = 0;
     sa.layout.g_count = count;
     if (times) check(cudaEventRecord(ev_[0], stream_), "cudaEventRecord");
-    spatial_pass(sa, sp.f64, true, times);
+    spatial_pass(sa, sp.f64, warp_s, times);
     if (times) check(cudaEventRecord(ev_[1], stream_), "cudaEventRecord");
     const int64_t nitems = (int64_t)rp.item_off.size() - 1;
     ddmk::TemporalArgs ta;
@@ -626,7 +650,8 @@ bool Engine::run_rings(const RunSpec& sp, const RingPlan& rp, double* d_means, P
     ta.ring.item_off = rc.item_off;
     ta.ring.partial = static_cast<double*>(buffer("ring_partial", (size_t)(nitems * N) * sizeof(double)));
     if (times) check(cudaEventRecord(ev_[2], stream_), "cudaEventRecord");
-    check(ddmk::launch_temporal_warp(ta, num_sms_, stream_), "temporal ring kernel");
+    check(warp_t ? ddmk::launch_temporal_warp(ta, num_sms_, stream_)
+                 : ddmk::launch_temporal_long(ta, num_sms_, nullptr, stream_), "temporal ring kernel");
     check(ddmk::launch_ring_means(ta.ring.partial, N, d_lag_index, rc.ring_item_off, rc.ring_bin,
                                   rc.ring_count, (int64_t)rp.ring_bin.size(), d_means, rp.nbins,
                                   stream_), "ring means kernel");

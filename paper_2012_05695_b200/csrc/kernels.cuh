@@ -119,6 +119,13 @@ size_t temporal_warp_smem();
 bool temporal_warp_segments_ok(const SegTable& segs, int N);
 cudaError_t launch_temporal_warp(const TemporalArgs& a, int num_sms, cudaStream_t stream);
 
+// CTA-per-sequence temporal engine (temporal_long.cu): f32, N2 in {4096, 8192}, layout T = 1
+// (or segments), map mode through a q-major staging block `out_q` of temporal_long_chunk(N)
+// sequences x N f32, or ring mode (RingArgs).
+bool temporal_long_supported(int N, int N2, int scalar_bytes);
+int64_t temporal_long_chunk(int N);
+cudaError_t launch_temporal_long(const TemporalArgs& a, int num_sms, void* out_q, cudaStream_t stream);
+
 // Register-resident spatial kernels (spatial_warp.cu): f32, power-of-two W/2 and H in
 // [16, 1024], u16/u8 frames, wave-vector-major output (layout T = 1).
 bool spatial_warp_supported(int W, int H, int pixel_bytes, int scalar_bytes);

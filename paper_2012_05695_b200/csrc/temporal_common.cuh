@@ -1,0 +1,96 @@
+// Shared device helpers of the temporal engines (temporal_warp.cu, temporal_long.cu):
+// TMA bulk copies with mbarrier completion and the register-resident length-1024 transform.
+#pragma once
+
+#include <cstdint>
+
+#include "kernels.cuh"
+#include "warp_fft.cuh"
+
+namespace ddmk {
+namespace tc {
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(unsigned long long* bar) {
+    asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(smem_addr(bar)));
+}
+
+// lane 0: expect `bytes` on `bar` and start the bulk copy global -> shared
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes,
+                                          unsigned long long* bar) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void fence_expect(unsigned long long* bar, uint32_t bytes) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t bytes,
+                                          unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t phase) {
+    asm volatile(
+        "{\n.reg .pred p;\nWAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
+        "r"(phase)
+        : "memory");
+}
+
+// v[b] *= W_64^{b} = exp(SIGN 2 pi i b / 64): compile-time constants after unrolling
+template <int SIGN>
+__device__ __forceinline__ void premul_w64(cpx<float> (&v)[32]) {
+#pragma unroll
+    for (int b = 1; b < 32; ++b) {
+        if (b == 16) v[b] = rot90<SIGN>(v[b]);  // W_64^{16} = SIGN i
+        else v[b] = cmul(v[b], ct_w<SIGN, float>(b, 64));
+    }
+}
+
+// Length-1024 transform of the warp (lane a holds x[a + 32 b] in v[b]; on return lane c
+// holds X[c + 32 d] in v[d]).  Four-step twiddles come from a CTA table twt[c][a]
+// (conflict-free 8-byte loads): W_1024^{a c}, or for ODD W_2048^{a (2c + 1)}, where the input
+// is x[n] W_2048^{n}: its W_64^{b} part is applied before the register DFT and its lane factor
+// W_2048^{a} is folded into the table, so X = the odd outputs of the zero-padded FFT_2048.
+template <int SIGN, bool ODD>
+__device__ __forceinline__ void fft1024(cpx<float> (&v)[32], cpx<float>* scratch, int lane,
+                                        const cpx<float>* __restrict__ twt) {
+    constexpr int P = 33;
+    if constexpr (ODD) premul_w64<SIGN>(v);
+    RegDft<32, SIGN, float>::run(v);
+#pragma unroll
+    for (int c = ODD ? 0 : 1; c < 32; ++c) {
+        cpx<float> w = twt[c * 32 + lane];
+        if (SIGN > 0) w.y = -w.y;
+        v[c] = cmul(v[c], w);
+    }
+#pragma unroll
+    for (int c = 0; c < 32; ++c) scratch[c * P + lane] = v[c];
+    __syncwarp();
+#pragma unroll
+    for (int ap = 0; ap < 32; ++ap) v[ap] = scratch[lane * P + ap];
+    __syncwarp();
+    RegDft<32, SIGN, float>::run(v);
+}
+
+
+}  // namespace tc
+}  // namespace ddmk

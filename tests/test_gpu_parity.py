@@ -356,3 +356,45 @@ def test_run_azimuthal_fused_equals_map_then_average(ddm):
     two_step, counts2 = ddm.azimuthal_average(arch.values, 256, 256)
     np.testing.assert_array_equal(counts, counts2)
     assert O.relative_l2(fused, two_step) <= 1e-6
+
+
+# --------------------------------------------------------------------------- long sequences
+# N2 = 4096 / 8192: the CTA-per-sequence engine (temporal_long.cu), map and ring modes.
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("W,H,N,q_max,lags", [
+    (32, 32, 1500, None, None),              # R = 4, generic spatial pass (T = 1 layout)
+    (64, 64, 2048, None, None),              # R = 4, N = L, register spatial pass
+    (16, 16, 2100, None, None),              # R = 8
+    (32, 24, 4096, 9.0, [0, 1, 2, 100, 4095]),  # R = 8, N = L, cutoff + lag subset
+])
+def test_long_sequences_vs_oracle(ddm, W, H, N, q_max, lags):
+    st = O.random_stack(W, H, N, seed=N)
+    cfg = ddm.RunConfig(precision="f32", memory_bytes=1 << 40, q_max=q_max,
+                        lags=lags if lags is not None else [])
+    got = ddm.run(st, cfg).values
+    ref = O.run_with_ft(st, "f32", lags=lags, q_max=q_max)
+    assert O.relative_l2(got, ref) <= 1e-4
+    li = np.asarray(O.normalize_lags(lags, N))
+    assert np.all(got[li == 0] == 0.0)
+
+
+@pytest.mark.gpu
+def test_long_sequences_groups_bitwise(ddm):
+    st = O.random_stack(32, 32, 1600, seed=4)
+    one = ddm.run(st, ddm.RunConfig(precision="f32", memory_bytes=1 << 40))
+    budget = 100 * 1600 * 8 + 32 * 17 * 8 + 4096 * 8   # ~100 wave vectors per group
+    many = ddm.run(st, ddm.RunConfig(precision="f32", memory_bytes=budget))
+    assert many.counters["spatial_ffts"] > one.counters["spatial_ffts"]
+    np.testing.assert_array_equal(one.values, many.values)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("W,H,N", [(64, 64, 2000), (32, 32, 3000)])
+def test_long_sequences_ring_average(ddm, W, H, N):
+    st = ddm.generate(W, H, N, particles=40, diffusion=0.5, seed=9)
+    cfg = ddm.RunConfig(precision="f32", memory_bytes=1 << 40)
+    means, counts, _ = ddm.run_azimuthal(st, cfg)
+    ref_means, ref_counts = O.azimuthal_average(O.run_with_ft(st, "f32"), W, H)
+    np.testing.assert_array_equal(counts, ref_counts)
+    assert O.relative_l2(means, ref_means) <= 1e-4

@@ -237,6 +237,8 @@ def test_gpu_virtual_ranks_c2_geometry(G):
     (64, 64, 128, 2, "f32", None),
     (64, 48, 100, 3, "f64", None),          # generic engines + repack path
     (30, 20, 33, 4, "f32", [0, 1, 5, 32]),  # odd N, odd tail segment, lag subset
+    (32, 32, 1500, 3, "f32", None),         # long-sequence engine reading segments (R = 4)
+    (16, 16, 2100, 8, "f32", [0, 3, 2099]), # long-sequence engine, R = 8
 ])
 def test_gpu_virtual_ranks_vs_oracle(W, H, N, G, precision, lags):
     st = O.random_stack(W, H, N, seed=77)
