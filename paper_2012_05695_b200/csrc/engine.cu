@@ -224,7 +224,12 @@ void Engine::spatial_pass(ddmk::SpatialArgs sa, bool f64, bool warp_s, PhaseTime
     const size_t per_frame = (size_t)(sa.W / 2 + 1) * sa.H * (f64 ? 16 : 8);
     // frame chunk whose row-pass output stays in L2 (~48 MB)
     int F = (int)std::max<int64_t>(1, std::min<int64_t>(N, (48u << 20) / per_frame));
-    if (warp_s && F > 32) F -= F % 32;  // whole frame groups per column CTA
+    if (warp_s) {
+        // whole column-CTA frame groups per chunk (full-length corner-turn runs), even when
+        // a large frame's chunk no longer fits L2 (2048^2: 8 frames = 134 MB)
+        const int Fc = ddmk::spatial_warp_col_frames(sa.H);
+        F = std::min(N, std::max(Fc, F - F % Fc));
+    }
     last_F_ = F;
     // register-resident path: the row pass of chunk k+1 runs beside the column pass of chunk
     // k on a second stream, through two L2-resident `mid` buffers

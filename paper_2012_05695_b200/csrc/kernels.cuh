@@ -129,6 +129,8 @@ cudaError_t launch_temporal_long(const TemporalArgs& a, int num_sms, void* out_q
 // Register-resident spatial kernels (spatial_warp.cu): f32, power-of-two W/2 and H in
 // [16, 1024], u16/u8 frames, wave-vector-major output (layout T = 1).
 bool spatial_warp_supported(int W, int H, int pixel_bytes, int scalar_bytes);
+// frames one column-pass CTA transforms together (the run length of its corner-turn stores)
+int spatial_warp_col_frames(int H);
 // parts: 1 = row pass (frames -> mid), 2 = column pass (mid -> spectra), 3 = both
 template <typename S>
 cudaError_t launch_spatial_warp(const SpatialArgs& a, cudaStream_t stream, int parts = 3);

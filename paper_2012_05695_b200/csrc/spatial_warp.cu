@@ -244,10 +244,15 @@ bool pow2_in(int x, int lo, int hi) { return x >= lo && x <= hi && (x & (x - 1))
 
 bool spatial_warp_supported(int W, int H, int pixel_bytes, int scalar_bytes) {
     if (scalar_bytes != 4 || (pixel_bytes != 1 && pixel_bytes != 2)) return false;
-    if (!(W % 2 == 0 && pow2_in(W / 2, 16, 1024) && pow2_in(H, 16, 1024))) return false;
+    if (!(W % 2 == 0 && pow2_in(W / 2, 16, 1024) && pow2_in(H, 16, 2048))) return false;
     const int e = 31 - __builtin_clz(W / 2);
     const int A = std::min(1 << (e / 2), 32);
     return H % (kThreads / A) == 0;  // whole row blocks per CTA
+}
+
+int spatial_warp_col_frames(int H) {
+    const int e = 31 - __builtin_clz(H);
+    return kThreads / std::min(1 << (e / 2), 32);
 }
 
 template <typename S>
@@ -272,6 +277,7 @@ cudaError_t launch_spatial_warp(const SpatialArgs& a, cudaStream_t stream, int p
     case LEN: launch_cols2<S, LEN>(a, stream); break;
     switch (a.H) {
         DDMK_C2(16) DDMK_C2(32) DDMK_C2(64) DDMK_C2(128) DDMK_C2(256) DDMK_C2(512) DDMK_C2(1024)
+        DDMK_C2(2048)
     default: return cudaErrorInvalidValue;
     }
 #undef DDMK_C2

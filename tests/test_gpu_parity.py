@@ -398,3 +398,14 @@ def test_long_sequences_ring_average(ddm, W, H, N):
     ref_means, ref_counts = O.azimuthal_average(O.run_with_ft(st, "f32"), W, H)
     np.testing.assert_array_equal(counts, ref_counts)
     assert O.relative_l2(means, ref_means) <= 1e-4
+
+
+@pytest.mark.gpu
+def test_tall_frames_column_pass(ddm):
+    """H = 2048 register column pass (the 2048^2 geometry), small width and frame count."""
+    st = O.random_stack(32, 2048, 40, seed=21)
+    got = ddm.run(st, ddm.RunConfig(precision="f32", memory_bytes=1 << 40)).values
+    assert O.relative_l2(got, O.run_with_ft(st, "f32")) <= 1e-4
+    sp = ddm.compute_spectra(st[:3], "f32")
+    ref = O.spectra(st[:3], "f64")
+    assert np.linalg.norm((sp - ref).ravel()) <= 1e-5 * np.linalg.norm(ref.ravel())
