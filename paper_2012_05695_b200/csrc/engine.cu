@@ -231,8 +231,38 @@ void Engine::spatial_pass(ddmk::SpatialArgs sa, bool f64, bool warp_s, PhaseTime
         F = std::min(N, std::max(Fc, F - F % Fc));
     }
     last_F_ = F;
-    // register-resident path: the row pass of chunk k+1 runs beside the column pass of chunk
-    // k on a second stream, through two L2-resident `mid` buffers
+    // register-resident path, preferred: one persistent launch schedules every row and
+    // column item of the step through a global queue (ring of nbuf L2-resident mid buffers)
+    // (opt-in: DDM_SPATIAL_FUSED=1; at 512^2 it trails the two-stream chunk pipeline below,
+    // 1.06 vs 0.92 ms, because one kernel's register budget caps the row items at 2 CTAs/SM)
+    static const char* fused_env = std::getenv("DDM_SPATIAL_FUSED");
+    const bool try_fused = warp_s && N > F && fused_env && fused_env[0] == '1';
+    if (try_fused) {
+        auto env_int = [](const char* name, int dflt) {
+            const char* e = std::getenv(name);
+            return e ? std::atoi(e) : dflt;
+        };
+        // rows run `lead` chunks ahead of the columns through a ring of nbuf = lead + 2 buffers
+        // of Ff frames (one column-CTA group each: full-length corner-turn runs), ~67 MB of L2
+        static const int lead = std::max(1, env_int("DDM_SPATIAL_LEAD", 2));
+        static const int nbuf = std::max(lead + 1, env_int("DDM_SPATIAL_NBUF", lead + 2));
+        const int Fc = ddmk::spatial_warp_col_frames(sa.H);
+        int Ff = std::max(Fc, env_int("DDM_SPATIAL_F", Fc));
+        Ff = std::min(N, Ff - Ff % Fc);
+        const int K = (N + Ff - 1) / Ff;
+        last_F_ = Ff;
+        sa.mid = mid_.ensure((size_t)Ff * per_frame * nbuf);
+        int* sync = static_cast<int*>(buffer("spatial_sync", (size_t)(1 + 2 * K) * sizeof(int)));
+        const cudaError_t e = ddmk::launch_spatial_fused(sa, Ff, nbuf, lead, sync, num_sms_, stream_);
+        if (e == cudaSuccess) {
+            if (times) times->spatial_launches += 1;
+            return;
+        }
+        if (e != cudaErrorNotSupported) check(e, "fused spatial kernel");
+        (void)cudaGetLastError();
+    }
+    // otherwise the row pass of chunk k+1 runs beside the column pass of chunk k on a second
+    // stream, through two L2-resident `mid` buffers
     const bool overlap = warp_s && N > F && std::getenv("DDM_SPATIAL_SERIAL") == nullptr;
     void* d_mid = mid_.ensure((size_t)F * per_frame * (overlap ? 2 : 1));
     sa.mid = d_mid;
