@@ -385,11 +385,18 @@ def our_arm(args, rank: int, world: int):
         e2e_step()
     e2e_steps = max(3, min(args.steps, 10))
     torch.cuda.synchronize()
+    phases = []
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
         e2e_step()
+        phases.append({f: float(getattr(timing, f)) for f, _ in ddm.Timing._fields_})
     torch.cuda.synchronize()
     e2e_s = (time.perf_counter() - t0) / e2e_steps
+    # the reference's TimingBreakdown of the C-ABI call, medians over the e2e steps (seconds):
+    # disk = pinned frames H2D, step1/step2 = device kernels, merge = f64 map D2H
+    e2e_phases = {f: statistics.median(p[f] for p in phases) for f in phases[0]}
+    h2d_gbps = st.nbytes / max(e2e_phases["disk"], 1e-9) / 1e9
+    d2h_gbps = N * plane * 8 / max(e2e_phases["merge"], 1e-9) / 1e9
     if dist:
         t = torch.tensor([e2e_s], device=f"cuda:{dev}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -432,6 +439,7 @@ def our_arm(args, rank: int, world: int):
         "clocks": clk.summary(),
         "e2e": {"value": world * N / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(st.nbytes),
                 "d2h_bytes_per_step": int(N * plane * 8), "ms_per_step": e2e_s * 1e3,
+                "phases_s": e2e_phases, "h2d_GBps": h2d_gbps, "d2h_GBps": d2h_gbps,
                 "path": "ddm_b200_run_u16 (C-ABI ddm::run): pinned u16 in, f64 lag-major map out"},
         "gpu_launches": launches,
     }
