@@ -313,16 +313,22 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
             OutT* dst = out + (int64_t)threadIdx.x * out_stride + q0;
             const int64_t step = (int64_t)blockDim.x * out_stride;
             if (vec_store) {
-#pragma unroll 2
-                for (int m = threadIdx.x; m < N; m += blockDim.x, dst += step) {
-                    float vv[kWarps];
-#pragma unroll
-                    for (int j = 0; j < kWarps; ++j)
-                        vv[j] = reinterpret_cast<const float*>(ws[j].scratch)[padded(m)];
-#pragma unroll
-                    for (int k = 0; k < kWarps / 4; ++k)
-                        reinterpret_cast<float4*>(dst)[k] =
-                            make_float4(vv[4 * k], vv[4 * k + 1], vv[4 * k + 2], vv[4 * k + 3]);
+                // thread pairs cover one lag row's kWarps * 4 = 32-byte run: lane 2i stores
+                // warps 0-3, lane 2i+1 warps 4-7, so each store instruction is 16 full
+                // 32-byte requests instead of 32 half ones
+                static_assert(kWarps == 8, "pair store assumes 8 wave vectors per tile");
+                const int h = threadIdx.x & 1;
+                const int rows = blockDim.x >> 1;
+                OutT* pdst = out + (int64_t)(threadIdx.x >> 1) * out_stride + q0 + 4 * h;
+                const int64_t pstep = (int64_t)rows * out_stride;
+#pragma unroll 4
+                for (int m = threadIdx.x >> 1; m < N; m += rows, pdst += pstep) {
+                    float4 v4;
+                    v4.x = reinterpret_cast<const float*>(ws[4 * h + 0].scratch)[padded(m)];
+                    v4.y = reinterpret_cast<const float*>(ws[4 * h + 1].scratch)[padded(m)];
+                    v4.z = reinterpret_cast<const float*>(ws[4 * h + 2].scratch)[padded(m)];
+                    v4.w = reinterpret_cast<const float*>(ws[4 * h + 3].scratch)[padded(m)];
+                    *reinterpret_cast<float4*>(pdst) = v4;
                 }
             } else {
                 for (int m = threadIdx.x; m < N; m += blockDim.x, dst += step) {
