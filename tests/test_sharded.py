@@ -246,3 +246,4 @@ def test_gpu_virtual_ranks_vs_oracle(W, H, N, G, precision, lags):
     ref = O.run_with_ft(st, precision, lags=lags)
     tol = 1e-4 if precision == "f32" else 1e-10
     assert O.relative_l2(got, ref) <= tol
+
