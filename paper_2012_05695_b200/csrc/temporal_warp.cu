@@ -189,6 +189,9 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
         __syncwarp();
         // the stage is free: start the next sequence's copy (it lands during three FFTs)
         after_reload();
+        // map mode: the previous tile's d values wait in every warp's pw until the CTA has
+        // stored them; the store overlaps this sequence's mean and even transform
+        if constexpr (!kRing) __syncthreads();
 #pragma unroll
         for (int b = 0; b < 32; ++b)
             my.pw[padded(lane + 32 * b)] = v[b].x * v[b].x + v[b].y * v[b].y;
@@ -304,7 +307,7 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
         const int64_t q = tile * kWarps + warp;
         const bool live = q < nq;
         process(q, live, [&] { prefetch_q(tile_q(tile + gridDim.x)); },
-                [&](int m, float val) { scf[padded(m)] = val; });
+                [&](int m, float val) { my.pw[padded(m)] = val; });   // S(m) was read into sv
 
         // ---- tile store: lag rows of kWarps consecutive wave vectors (32 B runs for f32)
         __syncthreads();
@@ -324,17 +327,17 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
 #pragma unroll 4
                 for (int m = threadIdx.x >> 1; m < N; m += rows, pdst += pstep) {
                     float4 v4;
-                    v4.x = reinterpret_cast<const float*>(ws[4 * h + 0].scratch)[padded(m)];
-                    v4.y = reinterpret_cast<const float*>(ws[4 * h + 1].scratch)[padded(m)];
-                    v4.z = reinterpret_cast<const float*>(ws[4 * h + 2].scratch)[padded(m)];
-                    v4.w = reinterpret_cast<const float*>(ws[4 * h + 3].scratch)[padded(m)];
+                    v4.x = ws[4 * h + 0].pw[padded(m)];
+                    v4.y = ws[4 * h + 1].pw[padded(m)];
+                    v4.z = ws[4 * h + 2].pw[padded(m)];
+                    v4.w = ws[4 * h + 3].pw[padded(m)];
                     *reinterpret_cast<float4*>(pdst) = v4;
                 }
             } else {
                 for (int m = threadIdx.x; m < N; m += blockDim.x, dst += step) {
 #pragma unroll
                     for (int j = 0; j < kWarps; ++j)
-                        dst[j] = (OutT) reinterpret_cast<const float*>(ws[j].scratch)[padded(m)];
+                        dst[j] = (OutT)ws[j].pw[padded(m)];
                 }
             }
         } else {
@@ -344,11 +347,11 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
                 const int li = lag_index ? lag_index[m] : m;
                 if (li < 0) continue;
                 const int64_t dst = dest_of_slot ? dest_of_slot[q0 + j] : q0 + j;
-                out[(int64_t)li * out_stride + dst] =
-                    (OutT) reinterpret_cast<const float*>(ws[j].scratch)[padded(m)];
+                out[(int64_t)li * out_stride + dst] = (OutT)ws[j].pw[padded(m)];
             }
         }
-        __syncthreads();
+        // no barrier here: the next sequence's transforms run while the stores drain; pw is
+        // rewritten only after the barrier inside process()
     }
 }
 
