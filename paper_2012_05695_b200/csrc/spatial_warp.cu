@@ -13,6 +13,7 @@
 //            vector receives F consecutive frames as one contiguous run:
 //            spec[slot * N + frame] (layout T = 1, consumed by temporal_warp.cu).
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 #include "kernels.cuh"
@@ -131,6 +132,65 @@ __device__ __forceinline__ void st_stream(cpx<S>* p, cpx<S> v) {
 // ---------------------------------------------------------------------------- cols
 // kCoherent: `mid` was written by other CTAs of the same launch (the fused spatial kernel),
 // so it is read through L2 (ld.global.cg), never a stale L1 line.
+// Column-pass epilogue: the CTA's transposed stage sm[r * (F + 1) + f] (wave-vector row r,
+// frame f of this CTA's nf frames starting at n0, column c) -> the spectra, a peer's receive
+// buffer, or a cutoff / group subset.
+template <typename S, int HL>
+__device__ __forceinline__ void cols_epilogue(const cpx<S>* sm, int Wh, int N, int n0, int nf, int c,
+                                              cpx<S>* __restrict__ spec, const SpecLayout& lay,
+                                              const int* __restrict__ slot_of_flat,
+                                              const PeerTable& peers) {
+    constexpr int A = split_a<HL>();
+    constexpr int F = kThreads / A;
+    constexpr int SP = F + 1;
+    const int64_t plane = (int64_t)HL * Wh;
+    if (peers.ranks > 0) {
+        // fused corner turn: every wave vector goes to its owner's receive buffer (a peer
+        // pointer over NVLink); rows ascend with j, so the owner index only moves forward
+        constexpr int RS = kThreads / F;
+        const int f = threadIdx.x % F, rb = threadIdx.x / F;
+        if (f < nf) {
+            const int64_t kstep = (int64_t)RS * Wh;
+            int64_t k = (int64_t)rb * Wh + c;
+            int d = 0;
+            int64_t k_end = -1;   // owner slice [.., k_end) of the current destination
+            cpx<S>* dst = nullptr;
+#pragma unroll 4
+            for (int j = 0; j < HL / RS; ++j, k += kstep, dst += kstep * N) {
+                if (k >= k_end) {  // crossed into the next rank's slice (rare)
+                    while (d + 1 < peers.ranks && k >= peers.q_begin[d + 1]) ++d;
+                    k_end = peers.q_begin[d + 1];
+                    dst = static_cast<cpx<S>*>(peers.base[d]) + (k - peers.q_begin[d]) * N + n0 + f;
+                }
+                st_stream(dst, sm[(rb + RS * j) * SP + f]);
+            }
+        }
+        return;
+    }
+    if (!slot_of_flat && lay.g_begin == 0 && lay.g_count == plane) {
+        // every wave vector of the plane, identity slots: thread (f, rb + RS j) copies one
+        // frame of wave vector (r, c); consecutive threads fill F-frame runs
+        constexpr int RS = kThreads / F;             // row stride
+        const int f = threadIdx.x % F, rb = threadIdx.x / F;
+        if (f < nf) {
+            cpx<S>* dst = spec + ((int64_t)rb * Wh + c) * N + n0 + f;
+            const int64_t step = (int64_t)RS * Wh * N;
+#pragma unroll 8
+            for (int j = 0; j < HL / RS; ++j) st_stream(dst + j * step, sm[(rb + RS * j) * SP + f]);
+        }
+        return;
+    }
+    for (int idx = threadIdx.x; idx < HL * F; idx += kThreads) {
+        const int r = idx / F, f = idx - r * F;
+        if (f >= nf) continue;
+        const int64_t flat = (int64_t)r * Wh + c;
+        const int64_t k = slot_of_flat ? (int64_t)slot_of_flat[flat] : flat;
+        const int64_t s = k - lay.g_begin;
+        if (k < 0 || s < 0 || s >= lay.g_count) continue;
+        spec[s * N + n0 + f] = sm[r * SP + f];
+    }
+}
+
 template <typename S, int HL, bool kCoherent>
 __device__ __forceinline__ void cols2_body(const cpx<S>* __restrict__ mid, int Wh, int N, int frame0,
                                            int nframes, const cpx<S>* __restrict__ tw_col,
@@ -185,53 +245,7 @@ __device__ __forceinline__ void cols2_body(const cpx<S>* __restrict__ mid, int W
     }
     __syncthreads();
 
-    const int n0 = frame0 + f0;
-    const int64_t plane = (int64_t)HL * Wh;
-    if (peers.ranks > 0) {
-        // fused corner turn: every wave vector goes to its owner's receive buffer (a peer
-        // pointer over NVLink); rows ascend with j, so the owner index only moves forward
-        constexpr int RS = kThreads / F;
-        const int f = threadIdx.x % F, rb = threadIdx.x / F;
-        if (f < nf) {
-            const int64_t kstep = (int64_t)RS * Wh;
-            int64_t k = (int64_t)rb * Wh + c;
-            int d = 0;
-            int64_t k_end = -1;   // owner slice [.., k_end) of the current destination
-            cpx<S>* dst = nullptr;
-#pragma unroll 4
-            for (int j = 0; j < HL / RS; ++j, k += kstep, dst += kstep * N) {
-                if (k >= k_end) {  // crossed into the next rank's slice (rare)
-                    while (d + 1 < peers.ranks && k >= peers.q_begin[d + 1]) ++d;
-                    k_end = peers.q_begin[d + 1];
-                    dst = static_cast<cpx<S>*>(peers.base[d]) + (k - peers.q_begin[d]) * N + n0 + f;
-                }
-                st_stream(dst, sm[(rb + RS * j) * SP + f]);
-            }
-        }
-        return;
-    }
-    if (!slot_of_flat && lay.g_begin == 0 && lay.g_count == plane) {
-        // every wave vector of the plane, identity slots: thread (f, rb + RS j) copies one
-        // frame of wave vector (r, c); consecutive threads fill F-frame runs
-        constexpr int RS = kThreads / F;             // row stride
-        const int f = threadIdx.x % F, rb = threadIdx.x / F;
-        if (f < nf) {
-            cpx<S>* dst = spec + ((int64_t)rb * Wh + c) * N + n0 + f;
-            const int64_t step = (int64_t)RS * Wh * N;
-#pragma unroll 8
-            for (int j = 0; j < HL / RS; ++j) st_stream(dst + j * step, sm[(rb + RS * j) * SP + f]);
-        }
-        return;
-    }
-    for (int idx = threadIdx.x; idx < HL * F; idx += kThreads) {
-        const int r = idx / F, f = idx - r * F;
-        if (f >= nf) continue;
-        const int64_t flat = (int64_t)r * Wh + c;
-        const int64_t k = slot_of_flat ? (int64_t)slot_of_flat[flat] : flat;
-        const int64_t s = k - lay.g_begin;
-        if (k < 0 || s < 0 || s >= lay.g_count) continue;
-        spec[s * N + n0 + f] = sm[r * SP + f];
-    }
+    cols_epilogue<S, HL>(sm, Wh, N, frame0 + f0, nf, c, spec, lay, slot_of_flat, peers);
 }
 
 template <typename S, int HL>
@@ -242,6 +256,15 @@ cols2_kernel(const cpx<S>* __restrict__ mid, int Wh, int N, int frame0, int nfra
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cols2_body<S, HL, false>(mid, Wh, N, frame0, nframes, tw_col, spec, lay, slot_of_flat, peers,
                              blockIdx.x, smem_raw);
+}
+
+// complex slots of the column pass's exchange / transpose area
+template <int HL>
+__host__ __device__ constexpr int cols_area() {
+    constexpr int A = split_a<HL>(), B = HL / A;
+    constexpr int ex = (kThreads / A) * B * (A + 1);
+    constexpr int st = HL * (kThreads / A + 1);
+    return ex > st ? ex : st;
 }
 
 template <int L>
