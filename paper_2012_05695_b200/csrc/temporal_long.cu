@@ -53,12 +53,14 @@ struct LongGeom {
     }
 };
 
-template <int R, bool kRing>
+// FULL: N == N2 / 2, every bound folds at compile time
+template <int R, bool kRing, bool FULL>
 __global__ void __launch_bounds__(32 * R, (R == 4 ? 2 : 1))
 temporal_long_kernel(const cpx<float>* __restrict__ spec, const __grid_constant__ SegTable segs,
-                     int N, int64_t q0, int64_t q1, float* __restrict__ out_q,
+                     int N_rt, int64_t q0, int64_t q1, float* __restrict__ out_q,
                      const __grid_constant__ RingArgs ring) {
     using G = LongGeom<R>;
+    const int N = FULL ? G::NMAX : N_rt;
     constexpr int T = G::T, H = G::H;
     extern __shared__ __align__(128) unsigned char smem[];
     unsigned char* p = smem;
@@ -206,13 +208,23 @@ temporal_long_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
 #pragma unroll
             for (int j = 0; j < H; ++j) {
                 const int n = n1 + kF * j;
-                if (n < N) {
+                if (FULL || n < N) {
                     const cpx<float> t = {stage[n].x - mx, stage[n].y - my};
-                    if (j == warp) pw[pad32(n)] = t.x * t.x + t.y * t.y;
                     a = (j == 0) ? t : cadd(a, cmul(t, wj[j]));
                 }
             }
             v[b] = cmul(cmul(a, tw_lane), tw_pre[warp * 32 + b]);
+        }
+        if (warp < H) {
+            // |t|^2 of chunk j = warp for the averages term (one warp-uniform branch)
+#pragma unroll
+            for (int b = 0; b < 32; ++b) {
+                const int n = lane + 32 * b + kF * warp;
+                if (FULL || n < N) {
+                    const float tx = stage[n].x - mx, ty = stage[n].y - my;
+                    pw[pad32(n)] = tx * tx + ty * ty;
+                }
+            }
         }
         __syncthreads();  // (B) the stage is free
         if (tid == 0) prefetch(qn);
@@ -333,7 +345,9 @@ cudaError_t launch_long(const TemporalArgs& a, int64_t q0, int64_t q1, float* ou
     const int64_t work = ring ? a.ring.nitems : q1 - q0;
     const int grid = (int)std::min<int64_t>(work, (int64_t)num_sms * per_sm);
     if (grid <= 0) return cudaSuccess;
-    auto k = ring ? temporal_long_kernel<R, true> : temporal_long_kernel<R, false>;
+    const bool full = a.N == G::NMAX;
+    auto k = ring ? (full ? temporal_long_kernel<R, true, true> : temporal_long_kernel<R, true, false>)
+                  : (full ? temporal_long_kernel<R, false, true> : temporal_long_kernel<R, false, false>);
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     k<<<grid, G::T, smem, stream>>>(static_cast<const cpx<float>*>(a.spec), a.segs, a.N, q0, q1, out_q,
