@@ -223,7 +223,15 @@ void Engine::spatial_pass(ddmk::SpatialArgs sa, bool f64, bool warp_s, PhaseTime
     const int N = sa.N;
     const size_t per_frame = (size_t)(sa.W / 2 + 1) * sa.H * (f64 ? 16 : 8);
     // frame chunk whose row-pass output stays in L2 (~48 MB)
-    int F = (int)std::max<int64_t>(1, std::min<int64_t>(N, (48u << 20) / per_frame));
+    // Frame chunk of the row pass. Measured at 512^2 x 1024 (tools/gpu_ab.sh, DDM_MID_MB):
+    // 32 frames (L2-resident mid) 0.88 ms, 80 frames 0.79 ms, 512 frames 0.76 ms. Launch and
+    // tail overhead per chunk outweighs L2 residency, so the register path takes two chunks
+    // (row pass of one overlapping the column pass of the other) up to 1 GiB per buffer.
+    static const char* mid_env = std::getenv("DDM_MID_MB");
+    const size_t mid_budget = mid_env ? (size_t)std::max(1, std::atoi(mid_env)) << 20
+                            : warp_s  ? std::min<size_t>((size_t)(N + 1) / 2 * per_frame, size_t(1) << 30)
+                                      : size_t(48) << 20;
+    int F = (int)std::max<int64_t>(1, std::min<int64_t>(N, mid_budget / per_frame));
     if (warp_s) {
         // whole column-CTA frame groups per chunk (full-length corner-turn runs), even when
         // a large frame's chunk no longer fits L2 (2048^2: 8 frames = 134 MB)
