@@ -2,8 +2,8 @@
 // Algorithm::WithFt runs on the GPU: frames are staged to HBM once, each wave-vector group
 // is one batched spatial pass + one fused temporal launch, results come back lag-major in
 // f64. Group planning, counters, partial files, before_merge and validation keep the
-// reference semantics. WithoutFt / Direct are not part of this accelerated path and raise
-// InputError (scope).
+// reference semantics. WithoutFt (the O(N * lags) spectral differences) and Direct (Eq. 1,
+// always f64) run on the GPU too, through the pairwise kernel (csrc/pairwise.cu).
 #ifndef DDM_B200_SCHEDULER_HPP
 #define DDM_B200_SCHEDULER_HPP
 
@@ -46,6 +46,20 @@ struct GroupPlan {
 };
 
 GroupPlan plan_with_ft(std::int64_t q_count, std::int64_t frames, const MemoryBudget& budget);
+
+/// WITHOUT_FT lag passes: a pass holds capacity - 1 consecutive lags' spectra ring
+/// (`plan_without_ft`, scheduler.cpp:386-411). On the device every pass shares one spatial
+/// step; the plan fixes the reference's counters and PlanError semantics.
+struct LagChunk {
+    std::int64_t lo = 0, hi = 0;
+    std::vector<std::int64_t> lags;
+};
+struct ChunkPlan {
+    std::int64_t capacity = 0;
+    std::vector<LagChunk> chunks;
+};
+ChunkPlan plan_without_ft(std::int64_t frames, std::vector<std::int64_t> lags,
+                          const MemoryBudget& budget, std::int64_t bytes_per_spectrum);
 
 /// Sharded WITH_FT over `ranks` GPUs (b200 extension). Rank r transforms
 /// frames [frame_begin[r], frame_begin[r+1]) in the spatial step and owns wave vectors

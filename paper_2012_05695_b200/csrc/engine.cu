@@ -712,6 +712,64 @@ bool Engine::run_rings(const RunSpec& sp, const RingPlan& rp, double* d_means, P
     return true;
 }
 
+void Engine::run_pairwise(const RunSpec& sp, PhaseTimes* times) {
+    check(cudaSetDevice(device_), "cudaSetDevice");
+    const int W = sp.W, H = sp.H, N = sp.N;
+    const int sb = sp.f64 ? 8 : 4;
+    const int64_t plane = (int64_t)H * (W / 2 + 1);
+    const int64_t count = (int64_t)sp.flat.size();
+    const int* d_slot = nullptr;
+    std::vector<int> slot_of;
+    if (!sp.identity) {
+        slot_of.assign((size_t)plane, -1);
+        for (size_t k = 0; k < sp.flat.size(); ++k) slot_of[(size_t)sp.flat[k]] = (int)k;
+        check(cudaMemcpyAsync(slotmap_.ensure((size_t)plane * sizeof(int)), slot_of.data(),
+                              (size_t)plane * sizeof(int), cudaMemcpyHostToDevice, stream_), "slot upload");
+        d_slot = static_cast<const int*>(slotmap_.get());
+    }
+    void* d_spec = spec_.ensure((size_t)count * N * 2 * sb);
+    const bool warp_s = !sp.f64 && ddmk::spatial_warp_supported(W, H, sp.pixel_bytes, sb) &&
+                        std::getenv("DDM_B200_V1_SPATIAL") == nullptr;
+    ddmk::SpatialArgs sa = spatial_args(sp.d_frames, sp.pixel_bytes, W, H, N, sp.f64);
+    sa.spec = d_spec;
+    sa.slot_of_flat = d_slot;
+    sa.layout.T = 1;
+    sa.layout.g_begin = 0;
+    sa.layout.g_count = count;
+    if (times) check(cudaEventRecord(ev_[0], stream_), "cudaEventRecord");
+    spatial_pass(sa, sp.f64, warp_s, times);
+    if (times) check(cudaEventRecord(ev_[1], stream_), "cudaEventRecord");
+    std::vector<int> lags(sp.lags.begin(), sp.lags.end());
+    int* d_lags = static_cast<int*>(buffer("pair_lags", std::max<size_t>(lags.size(), 1) * sizeof(int)));
+    check(cudaMemcpyAsync(d_lags, lags.data(), lags.size() * sizeof(int), cudaMemcpyHostToDevice, stream_),
+          "lag upload");
+    const int64_t* d_dest = nullptr;
+    if (!sp.identity) {
+        check(cudaMemcpyAsync(dest_.ensure((size_t)count * sizeof(int64_t)), sp.flat.data(),
+                              (size_t)count * sizeof(int64_t), cudaMemcpyHostToDevice, stream_),
+              "dest upload");
+        d_dest = static_cast<const int64_t*>(dest_.get());
+    }
+    if (times) check(cudaEventRecord(ev_[2], stream_), "cudaEventRecord");
+    check(sp.f64 ? ddmk::launch_pairwise<double>(d_spec, N, count, d_lags, (int)lags.size(),
+                                                 static_cast<double*>(sp.d_out), sp.out_stride, d_dest,
+                                                 num_sms_, stream_)
+                 : ddmk::launch_pairwise<float>(d_spec, N, count, d_lags, (int)lags.size(),
+                                                static_cast<double*>(sp.d_out), sp.out_stride, d_dest,
+                                                num_sms_, stream_),
+          "pairwise kernel");
+    if (times) check(cudaEventRecord(ev_[3], stream_), "cudaEventRecord");
+    check(cudaStreamSynchronize(stream_), "sync");   // host lag / slot vectors
+    if (times) {
+        float a = 0.f, b = 0.f;
+        cudaEventElapsedTime(&a, ev_[0], ev_[1]);
+        cudaEventElapsedTime(&b, ev_[2], ev_[3]);
+        times->spatial_ms += a;
+        times->temporal_ms += b;
+        times->temporal_launches += 1;
+    }
+}
+
 void Engine::spectra(const void* d_frames, int pixel_bytes, int W, int H, int N, bool f64,
                      void* d_out) {
     check(cudaSetDevice(device_), "cudaSetDevice");

@@ -136,6 +136,11 @@ public:
     bool run_rings(const RunSpec& spec, const RingPlan& rings, double* d_means,
                    PhaseTimes* times = nullptr);  // rings: from ring_plan()
 
+    // WITHOUT_FT (and Direct, given f64) over every retained wave vector: spatial pass into the
+    // wave-vector-major layout, then the pairwise kernel writing the f64 lag-major map
+    // (spec.d_out, spec.out_stride, identity or flat positions). Single group.
+    void run_pairwise(const RunSpec& spec, PhaseTimes* times = nullptr);
+
     // Device staging buffer for frames owned by the engine.
     void* frame_buffer(size_t bytes) { return frames_.ensure(bytes); }
     void* scratch(size_t bytes) { return user_scratch_.ensure(bytes); }

@@ -112,4 +112,25 @@ GroupPlan plan_with_ft(std::int64_t q_count, std::int64_t frames, const MemoryBu
     return plan;
 }
 
+ChunkPlan plan_without_ft(std::int64_t frames, std::vector<std::int64_t> lags,
+                          const MemoryBudget& budget, std::int64_t bytes_per_spectrum) {
+    // `scheduler.cpp:386-411`
+    if (bytes_per_spectrum < 1) throw InputError("plan_without_ft: bad spectrum size");
+    lags = normalize_lags(std::move(lags), frames);
+    const std::int64_t capacity = budget.bytes > 0 ? budget.bytes / bytes_per_spectrum : 0;
+    if (capacity < 2)
+        throw PlanError("memory budget " + std::to_string(budget.bytes) + " bytes admits fewer than two " +
+                        std::to_string(bytes_per_spectrum) + "-byte spectra");
+    ChunkPlan plan;
+    plan.capacity = capacity;
+    const std::int64_t width = capacity - 1;  // lags per pass
+    for (const std::int64_t lag : lags) {
+        if (lag == 0) continue;  // zero by definition, never scheduled
+        if (plan.chunks.empty() || lag > plan.chunks.back().lo + width - 1) plan.chunks.push_back({lag, lag, {}});
+        plan.chunks.back().hi = lag;
+        plan.chunks.back().lags.push_back(lag);
+    }
+    return plan;
+}
+
 }  // namespace ddm

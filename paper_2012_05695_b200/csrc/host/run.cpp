@@ -112,15 +112,87 @@ const void* stage_frames(b200::Engine& eng, const detail::Ingest& in, double& di
 
 namespace detail {
 
+// WITHOUT_FT (`scheduler.cpp:182-286`) and Direct (`:288-323`, always f64): one spatial step
+// and the pairwise kernel straight into the lag-major map. The reference's pass plan fixes the
+// counters (spatial_ffts = N x passes; pairs = sum over lags > 0 of N - m) and its PlanError.
+ResultArchive run_pairwise_core(const Ingest& in, const RunConfig& config,
+                                const std::vector<std::int64_t>& lags, const WaveVectorSet& wv,
+                                ResultArchive& archive,
+                                double* out, std::chrono::steady_clock::time_point wall0) {
+    const int W = in.width, H = in.height, N = in.frames;
+    const bool direct = config.algorithm == Algorithm::Direct;
+    const bool f64 = direct || config.precision == Precision::F64;
+    std::uint64_t pairs = 0;
+    for (const auto m : lags)
+        if (m > 0) pairs += std::uint64_t(N - m);
+    std::uint64_t passes = 0;
+    if (!direct) {
+        const MemoryBudget budget{config.memory_bytes, config.precision};
+        passes = plan_without_ft(N, lags, budget, spectrum_bytes(W, H, config.precision)).chunks.size();
+    }
+    if (std::int64_t(N) * 16 > 227 * 1024)
+        throw PlanError("sequence of " + std::to_string(N) + " frames exceeds the device pairwise "
+                        "engine limit of " + std::to_string(227 * 1024 / 16));
+    const std::int64_t plane = archive.map.plane_size();
+    const std::int64_t total = plane * std::int64_t(lags.size());
+
+    TimingBreakdown timing;
+    b200::Engine& eng = b200::Engine::instance(config.device);
+    std::lock_guard<std::mutex> lock(eng.mutex());
+    cudaStream_t st = eng.stream();
+    const void* d_frames = stage_frames(eng, in, timing.disk);
+
+    b200::RunSpec spec;
+    spec.W = W;
+    spec.H = H;
+    spec.N = N;
+    spec.f64 = f64;
+    spec.pixel_bytes = in.u8 ? 1 : 2;
+    spec.d_frames = d_frames;
+    spec.lags = lags;
+    spec.flat.resize(std::size_t(wv.count()));
+    spec.identity = true;
+    for (std::int64_t k = 0; k < wv.count(); ++k) {
+        spec.flat[std::size_t(k)] = wv.flat(k);
+        if (spec.flat[std::size_t(k)] != k) spec.identity = false;
+    }
+    spec.groups = {{0, wv.count()}};
+    double* d_map = static_cast<double*>(eng.buffer("map", std::size_t(total) * sizeof(double)));
+    if (!spec.identity)
+        b200::check(cudaMemsetAsync(d_map, 0, std::size_t(total) * sizeof(double), st), "memset");
+    spec.d_out = d_map;
+    spec.out_f64 = true;
+    spec.out_stride = plane;
+    b200::PhaseTimes times;
+    eng.run_pairwise(spec, &times);
+    bool finite = true;
+    double peak = 0.0, lowest = 0.0;
+    b200::reduce_stats(d_map, total, st, &finite, &peak, &lowest);
+    if (!finite) throw InputError("result map contains non-finite values");
+    const double eps = f64 ? 1e-9 : 1e-4;
+    if (lowest < -eps * std::max(peak, 1.0))
+        throw InputError("result map contains negative values beyond tolerance");
+    PhaseClock clock;
+    clock.start();
+    b200::check(cudaMemcpyAsync(out, d_map, std::size_t(total) * sizeof(double), cudaMemcpyDeviceToHost, st),
+                "map copy");
+    b200::check(cudaStreamSynchronize(st), "sync");
+    clock.stop(timing.merge);
+    timing.step1 = times.spatial_ms * 1e-3;
+    timing.step2 = times.temporal_ms * 1e-3;
+    archive.counters.spatial_ffts = direct ? pairs : std::uint64_t(N) * passes;
+    archive.counters.pairs = pairs;
+    timing.finish(std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count());
+    archive.timing = timing;
+    return archive;
+}
+
 ResultArchive run_core(const Ingest& in, const RunConfig& config, double* out,
                        std::int64_t capacity) {
     const auto wall0 = std::chrono::steady_clock::now();
     if (config.workers < 1) throw InputError("workers must be at least 1");
     if (in.frames < 1) throw InputError("stack has no frames");
     if (in.width < 1 || in.height < 1) throw InputError("frame dimensions must be positive");
-    if (config.algorithm != Algorithm::WithFt)
-        throw InputError("algorithm '" + to_string(config.algorithm) +
-                         "' is not part of the b200 accelerated path (with_ft only)");
     const int W = in.width, H = in.height, N = in.frames;
     const std::vector<std::int64_t> lags =
         config.lags.empty() ? all_lags(N) : normalize_lags(config.lags, N);
@@ -131,7 +203,7 @@ ResultArchive run_core(const Ingest& in, const RunConfig& config, double* out,
     ResultArchive archive;
     archive.frames = N;
     archive.algorithm = to_string(config.algorithm);
-    archive.precision = to_string(config.precision);
+    archive.precision = config.algorithm == Algorithm::Direct ? "f64" : to_string(config.precision);
     archive.q_max = config.q_max;
     archive.workers = config.workers;
     archive.map.width = W;
@@ -141,6 +213,9 @@ ResultArchive run_core(const Ingest& in, const RunConfig& config, double* out,
     const std::int64_t plane = archive.map.plane_size();
     const std::int64_t total = plane * std::int64_t(lags.size());
     if (capacity < total) throw InputError("output capacity is smaller than lags x plane");
+
+    if (config.algorithm != Algorithm::WithFt)
+        return run_pairwise_core(in, config, lags, wv, archive, out, wall0);
 
     // budget floor + group plan (`scheduler.cpp:73-84`, `:365-384`)
     const MemoryBudget budget{config.memory_bytes, config.precision};

@@ -107,6 +107,13 @@ cudaError_t launch_ring_means(const double* partial, int N, const int* lag_index
                               const int64_t* ring_count, int64_t nrings, double* means,
                               int64_t nbins, cudaStream_t stream);
 
+// WITHOUT_FT (`pairwise.cpp:11-72`): spec wave-vector-major [q][N] in the working precision,
+// lags ascending (n_lags entries, 0 allowed), out[li * out_stride + dest(q)] f64.
+template <typename S>
+cudaError_t launch_pairwise(const void* spec, int N, int64_t nq, const int* lags, int n_lags,
+                            double* out, int64_t out_stride, const int64_t* dest_of_slot,
+                            int num_sms, cudaStream_t stream);
+
 // Segmented sequences (SegTable over q_count sequences) -> the engine's tile-major layout T.
 template <typename S>
 cudaError_t launch_repack_segments(const void* recv, int64_t q_count, const SegTable& segs, int N,

@@ -233,7 +233,8 @@ def run(stack, config: RunConfig, frame_interval: float = 1.0) -> ResultArchive:
     _check(rc)
     k = n_lags.value
     return ResultArchive(values[: k * plane].reshape(k, h, half_cols(w)), out_lags[:k].copy(), w, h,
-                         n, frame_interval, config.algorithm, config.precision, config.q_max,
+                         n, frame_interval, config.algorithm,
+                         "f64" if config.algorithm == "direct" else config.precision, config.q_max,
                          config.workers,
                          {f: int(getattr(counters, f)) for f, _ in Counters._fields_},
                          {f: float(getattr(timing, f)) for f, _ in Timing._fields_})

@@ -95,9 +95,46 @@ def main() -> None:
                                                               diffusion=d, seed=seed)
     np.savez_compressed(OUT / "synth.npz", **syn)
 
+    pairwise()
+
     for f in sorted(OUT.glob("*.npz")):
         print(f.name, f.stat().st_size)
 
 
+def pairwise() -> None:
+    """WITHOUT_FT and Direct maps + counters from the reference (pairwise.npz)."""
+    out = {}
+    for (w, h, n, seed, lagmode) in STACKS:
+        key = f"{w}x{h}x{n}_s{seed}"
+        st = O.random_stack(w, h, n, seed)
+        lags = O.log_lags(n) if lagmode == "log" else []
+        for prec in ("f64", "f32"):
+            r = ref.run(st, "without_ft", prec, lags=lags, workers=4)
+            out[f"without_{prec}_{key}"] = r.values
+            out[f"without_{prec}_counters_{key}"] = np.asarray(
+                [r.counters["spatial_ffts"], r.counters["temporal_ffts"], r.counters["pairs"]], np.int64)
+        r = ref.run(st, "direct", "f32", lags=lags, workers=4)
+        out[f"direct_{key}"] = r.values
+        out[f"direct_counters_{key}"] = np.asarray(
+            [r.counters["spatial_ffts"], r.counters["temporal_ffts"], r.counters["pairs"]], np.int64)
+    # pass plan (`test_scheduler.cpp:182-197`): 16x16x64 seed 107 with budgets of 1 and 3 passes
+    st = O.random_stack(16, 16, 64, 107)
+    sb = 16 * 9 * 16
+    for passes, cap in ((1, 64), (3, 22)):
+        r = ref.run(st, "without_ft", "f64", memory_bytes=cap * sb, workers=2)
+        out[f"passes{passes}_map"] = r.values
+        out[f"passes{passes}_counters"] = np.asarray(
+            [r.counters["spatial_ffts"], r.counters["temporal_ffts"], r.counters["pairs"]], np.int64)
+        out[f"passes{passes}_budget"] = np.asarray([cap * sb], np.int64)
+    # q_max cutoff + lag subset on without_ft
+    st = O.random_stack(24, 20, 40, 211)
+    r = ref.run(st, "without_ft", "f64", lags=[0, 1, 5, 39], q_max=6.5, workers=2)
+    out["cut_map"] = r.values
+    np.savez_compressed(OUT / "pairwise.npz", **out)
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["pairwise"]:
+        pairwise()
+    else:
+        main()

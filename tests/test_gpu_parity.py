@@ -432,3 +432,60 @@ def test_smoke_entry_point():
     """__graft_entry__.smoke(): the driver's round-end check runs and passes."""
     import __graft_entry__ as g
     g.smoke()
+
+
+# --------------------------------------------------------------------------- WITHOUT_FT / Direct
+
+PAIR_STACKS = [(8, 8, 16, 101, None), (16, 16, 64, 103, None), (25, 20, 30, 11, None),
+               (1, 1, 5, 3, None), (3, 5, 7, 4, None), (6, 10, 12, 5, None),
+               (32, 32, 100, 7, None), (50, 50, 100, 9, "log"), (64, 48, 200, 13, "log")]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("w,h,n,seed,lagmode", PAIR_STACKS)
+def test_without_ft_and_direct_vs_reference(ddm, w, h, n, seed, lagmode):
+    """The reference's own WITHOUT_FT (f64, f32) and Direct maps and counters
+    (tests/golden/pairwise.npz) from the device pairwise kernel."""
+    g = np.load(GOLD / "pairwise.npz")
+    key = f"{w}x{h}x{n}_s{seed}"
+    st = O.random_stack(w, h, n, seed)
+    lags = O.log_lags(n) if lagmode == "log" else []
+    for alg, prec, tag in (("without_ft", "f64", "without_f64"), ("without_ft", "f32", "without_f32"),
+                           ("direct", "f32", "direct")):
+        a = ddm.run(st, ddm.RunConfig(algorithm=alg, precision=prec, lags=lags, memory_bytes=1 << 40))
+        ref = g[f"{tag}_{key}"]
+        counters = g[f"{tag}_counters_{key}" if tag != "direct" else f"direct_counters_{key}"]
+        tol = 1e-12 if tag == "without_f64" else (1e-9 if tag == "direct" else 1e-5)
+        assert O.relative_deviation(a.values, ref) <= tol, tag
+        assert [a.counters["spatial_ffts"], a.counters["temporal_ffts"], a.counters["pairs"]] == list(counters)
+        if alg == "direct":
+            assert a.precision == "f64"
+
+
+@pytest.mark.gpu
+def test_without_ft_pass_plan_and_cutoff(ddm):
+    g = np.load(GOLD / "pairwise.npz")
+    st = O.random_stack(16, 16, 64, 107)
+    for passes in (1, 3):
+        a = ddm.run(st, ddm.RunConfig(algorithm="without_ft", precision="f64",
+                                      memory_bytes=int(g[f"passes{passes}_budget"][0])))
+        assert [a.counters["spatial_ffts"], a.counters["temporal_ffts"], a.counters["pairs"]] == \
+            list(g[f"passes{passes}_counters"])
+        assert O.relative_deviation(a.values, g[f"passes{passes}_map"]) <= 1e-12
+    with pytest.raises(ddm.PlanError):
+        ddm.run(st, ddm.RunConfig(algorithm="without_ft", precision="f64", memory_bytes=16 * 9 * 16))
+    st = O.random_stack(24, 20, 40, 211)
+    a = ddm.run(st, ddm.RunConfig(algorithm="without_ft", precision="f64", lags=[0, 1, 5, 39], q_max=6.5,
+                                  memory_bytes=1 << 40))
+    np.testing.assert_allclose(a.values, g["cut_map"], rtol=1e-12, atol=0)
+
+
+@pytest.mark.gpu
+def test_without_ft_agrees_with_with_ft_at_c2(ddm):
+    """The paper's two algorithms on the headline geometry (log lags), f64 and f32."""
+    st = ddm.generate(512, 512, 1024, particles=100, diffusion=0.5, seed=7)
+    lags = O.log_lags(1024)
+    for prec, tol in (("f64", 1e-10), ("f32", 1e-4)):
+        wo = ddm.run(st, ddm.RunConfig(algorithm="without_ft", precision=prec, lags=lags, memory_bytes=1 << 40))
+        wf = ddm.run(st, ddm.RunConfig(precision=prec, lags=lags, memory_bytes=1 << 40))
+        assert O.relative_l2(wo.values, wf.values) <= tol

@@ -143,3 +143,20 @@ def test_oracle_against_live_reference():
         r = ref.run(st, "with_ft", prec, workers=3)
         assert O.relative_deviation(O.run_with_ft(st, prec), r.values) <= (1e-12 if prec == "f64" else 1e-5)
         assert r.counters["temporal_ffts"] == 2 * 10 * 7
+
+
+def test_pairwise_goldens_pin_the_oracle():
+    """WITHOUT_FT / Direct maps produced by the reference (tests/golden/pairwise.npz) against
+    the numpy restatement (`pairwise.cpp:11-116`)."""
+    g = np.load(GOLD / "pairwise.npz")
+    for (w, h, n, seed, lagmode) in [(8, 8, 16, 101, None), (25, 20, 30, 11, None),
+                                     (50, 50, 100, 9, "log")]:
+        key = f"{w}x{h}x{n}_s{seed}"
+        st = O.random_stack(w, h, n, seed)
+        lags = O.log_lags(n) if lagmode == "log" else None
+        ref = g[f"without_f64_{key}"]
+        assert O.relative_deviation(O.run_without_ft(st, "f64", lags=lags), ref) <= 1e-12
+        # Eq. 1 equals the spectral differences (linearity of the transform)
+        assert O.relative_deviation(g[f"direct_{key}"], ref) <= 1e-9
+        pairs = sum(n - m for m in O.normalize_lags(lags, n) if m > 0)
+        assert g[f"direct_counters_{key}"][2] == pairs
