@@ -65,32 +65,62 @@ __device__ __forceinline__ void premul_w64(cpx<float> (&v)[32]) {
     }
 }
 
+// Exchange pitch of the length-1024 transforms: 34 complex per row keeps every row 16-byte
+// aligned, so the transposed reads are 128-bit (two values per load) and stay conflict-free
+// per quarter warp; a warp's exchange buffer holds kXS complex.
+constexpr int kXP = 34;
+constexpr int kXS = 32 * kXP;
+
 // Length-1024 transform of the warp (lane a holds x[a + 32 b] in v[b]; on return lane c
-// holds X[c + 32 d] in v[d]).  Four-step twiddles come from a CTA table twt[c][a]
-// (conflict-free 8-byte loads): W_1024^{a c}, or for ODD W_2048^{a (2c + 1)}, where the input
+// holds X[c + 32 d] in v[d]).  Four-step twiddles come from a CTA table twt[a * kXP + c]
+// (lane-major, 128-bit loads): W_1024^{a c}, or for ODD W_2048^{a (2c + 1)}, where the input
 // is x[n] W_2048^{n}: its W_64^{b} part is applied before the register DFT and its lane factor
 // W_2048^{a} is folded into the table, so X = the odd outputs of the zero-padded FFT_2048.
 template <int SIGN, bool ODD>
 __device__ __forceinline__ void fft1024(cpx<float> (&v)[32], cpx<float>* scratch, int lane,
                                         const cpx<float>* __restrict__ twt) {
-    constexpr int P = 33;
     if constexpr (ODD) premul_w64<SIGN>(v);
     RegDft<32, SIGN, float>::run(v);
+    const float4* tw4 = reinterpret_cast<const float4*>(twt + lane * kXP);
 #pragma unroll
-    for (int c = ODD ? 0 : 1; c < 32; ++c) {
-        cpx<float> w = twt[c * 32 + lane];
-        if (SIGN > 0) w.y = -w.y;
-        v[c] = cmul(v[c], w);
+    for (int c = 0; c < 32; c += 2) {
+        const float4 t = tw4[c / 2];
+        cpx<float> w0 = {t.x, t.y}, w1 = {t.z, t.w};
+        if (SIGN > 0) {
+            w0.y = -w0.y;
+            w1.y = -w1.y;
+        }
+        if (ODD || c > 0) v[c] = cmul(v[c], w0);
+        v[c + 1] = cmul(v[c + 1], w1);
     }
 #pragma unroll
-    for (int c = 0; c < 32; ++c) scratch[c * P + lane] = v[c];
+    for (int c = 0; c < 32; ++c) scratch[c * kXP + lane] = v[c];
     __syncwarp();
+    const float4* row = reinterpret_cast<const float4*>(scratch + lane * kXP);
 #pragma unroll
-    for (int ap = 0; ap < 32; ++ap) v[ap] = scratch[lane * P + ap];
+    for (int ap = 0; ap < 32; ap += 2) {
+        const float4 t = row[ap / 2];
+        v[ap] = {t.x, t.y};
+        v[ap + 1] = {t.z, t.w};
+    }
     __syncwarp();
     RegDft<32, SIGN, float>::run(v);
 }
 
+// Twiddle tables of fft1024 (kXS complex each): even W_1024^{a c}, odd W_2048^{a (2c + 1)}
+__device__ __forceinline__ void fill_fft1024_tables(cpx<float>* tw_even, cpx<float>* tw_odd,
+                                                    int tid, int nthreads) {
+    for (int i = tid; i < 32 * 32; i += nthreads) {
+        const int a = i >> 5, c = i & 31;
+        double sn, cs;
+        sincospi(-2.0 * (double)(a * c) / 1024, &sn, &cs);
+        tw_even[a * kXP + c] = {(float)cs, (float)sn};
+        if (tw_odd) {
+            sincospi(-2.0 * (double)(a * (2 * c + 1)) / 2048, &sn, &cs);
+            tw_odd[a * kXP + c] = {(float)cs, (float)sn};
+        }
+    }
+}
 
 }  // namespace tc
 }  // namespace ddmk

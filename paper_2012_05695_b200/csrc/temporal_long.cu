@@ -31,7 +31,7 @@ namespace {
 using namespace tc;
 
 constexpr int kF = 1024;
-constexpr int kFPad = kF + kF / 32;
+constexpr int kFPad = kXS;                 // exchange buffer per warp (pitch kXP)
 
 __device__ __forceinline__ int pad32(int n) { return n + (n >> 5); }
 
@@ -44,7 +44,7 @@ struct LongGeom {
     static constexpr size_t pw = (size_t)(NMAX + NMAX / 32) * 4;
     static constexpr size_t scratch = (size_t)R * kFPad * 8;
     static constexpr size_t acc = pw;
-    static constexpr size_t tw_even = 32 * 32 * 8;
+    static constexpr size_t tw_even = (size_t)kXS * 8;
     static constexpr size_t tw_pre = (size_t)R * 32 * 8;
     static constexpr size_t comb_d = (size_t)H * 32 * 8;
     static constexpr size_t red = 64 * 8;
@@ -79,12 +79,7 @@ temporal_long_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     cpx<float>* my_scratch = scratch + warp * kFPad;
 
-    for (int i = tid; i < 32 * 32; i += T) {
-        const int c = i >> 5, a = i & 31;
-        double sn, cs;
-        sincospi(-2.0 * (double)(a * c) / kF, &sn, &cs);
-        tw_even[i] = {(float)cs, (float)sn};
-    }
+    fill_fft1024_tables(tw_even, nullptr, tid, T);
     for (int i = tid; i < R * 32; i += T) {
         const int r = i >> 5, b = i & 31;
         double sn, cs;

@@ -44,7 +44,7 @@ __device__ __forceinline__ int padded(int n) { return n + (n >> 5); }
 //   scratch : exchange buffer of the three FFTs, then the f32 lag values of the tile store
 struct WarpSmem {
     cpx<float> stage[kPad];
-    cpx<float> scratch[kPad];
+    cpx<float> scratch[kXS];     // FFT exchange (pitch kXP)
     float pw[kPad];              // |t|^2, then S(m): frees the stage for the next copy early
     unsigned long long bar;
     unsigned long long pad_;
@@ -64,9 +64,9 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
     const int N = FULL ? kL : N_rt;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     WarpSmem* ws = reinterpret_cast<WarpSmem*>(smem_raw);
-    cpx<float>* tw_even = reinterpret_cast<cpx<float>*>(ws + kWarps);  // [c][a] W_1024^{a c}
-    cpx<float>* tw_odd = tw_even + 32 * 32;                              // [c][a] W_2048^{a (2c+1)}
-    float* rcp = reinterpret_cast<float*>(tw_odd + 32 * 32);             // 1 / (N - m)
+    cpx<float>* tw_even = reinterpret_cast<cpx<float>*>(ws + kWarps);  // [a][c] W_1024^{a c}
+    cpx<float>* tw_odd = tw_even + kXS;                                  // [a][c] W_2048^{a (2c+1)}
+    float* rcp = reinterpret_cast<float*>(tw_odd + kXS);                 // 1 / (N - m)
     float* acc_base = rcp + kL;                                          // kRing: [warp][kPad]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -78,14 +78,7 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
         mbar_init(&my.bar);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    for (int i = threadIdx.x; i < 32 * 32; i += blockDim.x) {
-        const int c = i >> 5, a = i & 31;
-        double sn, cs;
-        sincospi(-2.0 * (double)(a * c) / kL, &sn, &cs);
-        tw_even[i] = {(float)cs, (float)sn};
-        sincospi(-2.0 * (double)(a * (2 * c + 1)) / kN2, &sn, &cs);
-        tw_odd[i] = {(float)cs, (float)sn};
-    }
+    fill_fft1024_tables(tw_even, tw_odd, threadIdx.x, blockDim.x);
     cpx<float> base_unf;  // W_N2^{-lane}
     {
         double sn, cs;
@@ -370,7 +363,7 @@ constexpr int kTW = 8;
 template <typename OutT, bool kDiag, bool kRing>
 cudaError_t launch_w(const TemporalArgs& a, int num_sms, cudaStream_t stream) {
     constexpr int W = kTW;
-    const size_t smem = sizeof(WarpSmem) * W + 2 * 32 * 32 * sizeof(cpx<float>) + kL * sizeof(float) +
+    const size_t smem = sizeof(WarpSmem) * W + 2 * kXS * sizeof(cpx<float>) + kL * sizeof(float) +
                         (kRing ? (size_t)W * kPad * sizeof(float) : 0);
     const int64_t work = kRing ? a.ring.nitems : (a.layout.g_count + W - 1) / W;
     const int grid = (int)std::min<int64_t>(work, (int64_t)num_sms);
@@ -389,7 +382,7 @@ cudaError_t launch_w(const TemporalArgs& a, int num_sms, cudaStream_t stream) {
 }  // namespace
 
 size_t temporal_warp_smem() {
-    return sizeof(WarpSmem) * kTW + 2 * 32 * 32 * sizeof(cpx<float>) + kL * sizeof(float);
+    return sizeof(WarpSmem) * kTW + 2 * kXS * sizeof(cpx<float>) + kL * sizeof(float);
 }
 
 bool temporal_warp_segments_ok(const SegTable& segs, int N) {
