@@ -187,6 +187,20 @@ int ddm_b200_run_azimuthal_u16(const uint16_t* pixels, int width, int height, in
                                int64_t* counts, int64_t* bin_count, int64_t* out_lags,
                                int64_t* out_n_lags);
 
+/* ddm::fit_all_bins / fit_exponential (analysis.cpp:108-224): d = A (1 - exp(-t / tau)) + B per
+   ring, t = lag * frame_interval, over the lags >= 1 with finite means; means is the
+   [n_lags][nbins] ring profile (as ddm_b200_azimuthal / run_azimuthal produce).  One warp per
+   ring on the device.  Outputs are per bin (host arrays of nbins); flag 0 ok, 1 degenerate,
+   2 no_converge, -1 not fitted (empty ring or fewer than 4 usable lags). */
+int ddm_b200_fit_rings(const double* means, const int64_t* lags, int64_t n_lags,
+                       const int64_t* counts, int64_t nbins, double frame_interval, int device,
+                       double* amplitude, double* baseline, double* tau, double* residual,
+                       int* flag);
+/* ddm::estimate_diffusion (analysis.cpp:242-271) over the ok fits of bins [q_lo, q_hi]. */
+int ddm_b200_estimate_diffusion(const double* tau, const int* flag, int64_t nbins, int64_t width,
+                                int64_t q_lo, int64_t q_hi, double* coefficient,
+                                int64_t* bins_used);
+
 /* ddm::generate (proj/core/src/synth.cpp:98-132), bit-identical u16 frames. */
 int ddm_b200_generate(int64_t particles, double diffusion, double psf_sigma, double amplitude,
                       double background, int width, int height, int frames,

@@ -292,3 +292,84 @@ def ramp_check() -> bool:
 
 def frames_per_second(frames: int, seconds: float) -> float:
     return frames / seconds if seconds > 0 else math.inf
+
+
+# --------------------------------------------------------------------------- relaxation fits
+
+
+def fit_exponential(t: np.ndarray, y: np.ndarray, frame_interval: float = 1.0):
+    """`analysis.cpp:108-224`: Levenberg-Marquardt of y = A (1 - exp(-t / tau)) + B over
+    (A, B, ln tau), sequential sums as the reference. Returns (A, B, tau, residual, flag) with
+    flag 'ok' | 'degenerate' | 'no_converge'."""
+    t = np.asarray(t, dtype=np.float64)
+    y = np.asarray(y, dtype=np.float64)
+    if t.size < 4:
+        raise ValueError("fit_exponential: need at least 4 usable lags")
+    y_max, y_min = float(y.max()), float(y.min())
+    scale = max(abs(y_max), abs(y_min), 1e-300)
+    if y_max - y_min <= 1e-12 * scale:
+        return 0.0, float(np.sum(y)) / y.size, frame_interval, 0.0, "degenerate"
+
+    def cost(a, b, tau):
+        s = 0.0
+        for ti, yi in zip(t, y):
+            r = a * (1.0 - np.exp(-ti / tau)) + b - yi
+            s += r * r
+        return s
+
+    a, b = y_max, 0.0
+    knee = a * (1.0 - np.exp(-1.0))
+    tau = float(t[int(np.argmin(np.abs(y - knee)))])
+    lam = 1e-3
+    c = cost(a, b, tau)
+    converged = False
+    for _ in range(200):
+        jtj = np.zeros((3, 3))
+        jtr = np.zeros(3)
+        for ti, yi in zip(t, y):
+            e = np.exp(-ti / tau)
+            r = a * (1.0 - e) + b - yi
+            j = np.array([1.0 - e, 1.0, -a * e * ti / tau])
+            jtj += np.outer(j, j)
+            jtr += j * r
+        damped = jtj.copy()
+        for p in range(3):
+            damped[p, p] += lam * max(jtj[p, p], 1e-300)
+        try:
+            if np.min(np.abs(np.linalg.eigvals(damped))) < 1e-300:
+                raise np.linalg.LinAlgError
+            step = np.linalg.solve(damped, -jtr)
+        except np.linalg.LinAlgError:
+            lam *= 5.0
+            continue
+        a2, b2 = a + step[0], b + step[1]
+        tau2 = tau * np.exp(np.clip(step[2], -5.0, 5.0))
+        c2 = cost(a2, b2, tau2)
+        if c2 <= c:
+            gain = c - c2
+            a, b, tau, c = a2, b2, tau2, c2
+            lam = max(lam / 3.0, 1e-12)
+            if gain <= 1e-14 * (c + 1e-300):
+                converged = True
+                break
+        else:
+            lam *= 5.0
+            if lam > 1e12:
+                converged = True
+                break
+    return a, b, tau, float(np.sqrt(c / t.size)), "ok" if converged else "no_converge"
+
+
+def estimate_diffusion(fits, width: int, q_lo: int, q_hi: int):
+    """`analysis.cpp:242-271`: D from 1/tau = D q^2 (through the origin), q = 2 pi bin / width,
+    over the 'ok' fits of bins [q_lo, q_hi]. fits: {bin: (A, B, tau, residual, flag)}."""
+    sxx = sxy = 0.0
+    used = 0
+    for b, (_, _, tau, _, flag) in fits.items():
+        if flag != "ok" or b < q_lo or b > q_hi:
+            continue
+        x = (2.0 * np.pi * b / width) ** 2
+        sxx += x * x
+        sxy += x / tau
+        used += 1
+    return (sxy / sxx if used and sxx > 0 else 0.0), used

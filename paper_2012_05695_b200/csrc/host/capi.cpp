@@ -11,6 +11,7 @@
 #include "run_internal.hpp"
 
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <new>
 #include <optional>
@@ -507,6 +508,67 @@ int ddm_b200_run_azimuthal_u16(const uint16_t* pixels, int width, int height, in
             ddm::b200::check(cudaStreamSynchronize(eng.stream()), "sync");
             return 0;
         });
+    });
+}
+
+int ddm_b200_fit_rings(const double* means, const int64_t* lags, int64_t n_lags,
+                       const int64_t* counts, int64_t nbins, double frame_interval, int device,
+                       double* amplitude, double* baseline, double* tau, double* residual,
+                       int* flag) {
+    return guarded([&] {
+        if (!means || !lags || !counts || !amplitude || !baseline || !tau || !residual || !flag)
+            throw ddm::InputError("null buffer");
+        if (n_lags < 1 || nbins < 1) throw ddm::InputError("empty profile");
+        if (!(frame_interval > 0.0)) throw ddm::InputError("frame interval must be positive");
+        ddm::detail::guard_device([&] {
+            auto& eng = ddm::b200::Engine::instance(device);
+            std::lock_guard<std::mutex> lock(eng.mutex());
+            cudaStream_t st = eng.stream();
+            const size_t L = size_t(n_lags), B = size_t(nbins);
+            char* base = static_cast<char*>(eng.buffer("fit_io", L * B * 8 + L * 8 + B * 8 + 4 * B * 8 + B * 4));
+            double* d_means = reinterpret_cast<double*>(base);
+            int64_t* d_lags = reinterpret_cast<int64_t*>(d_means + L * B);
+            int64_t* d_counts = d_lags + L;
+            double* d_out = reinterpret_cast<double*>(d_counts + B);
+            int* d_flag = reinterpret_cast<int*>(d_out + 4 * B);
+            ddm::b200::check(cudaMemcpyAsync(d_means, means, L * B * 8, cudaMemcpyHostToDevice, st), "upload");
+            ddm::b200::check(cudaMemcpyAsync(d_lags, lags, L * 8, cudaMemcpyHostToDevice, st), "upload");
+            ddm::b200::check(cudaMemcpyAsync(d_counts, counts, B * 8, cudaMemcpyHostToDevice, st), "upload");
+            ddm::b200::check(ddmk::launch_fit_rings(d_means, d_lags, int(n_lags), d_counts, nbins, frame_interval,
+                                                    d_out, d_out + B, d_out + 2 * B, d_out + 3 * B, d_flag, st),
+                             "fit kernel");
+            ddm::b200::check(cudaMemcpyAsync(amplitude, d_out, B * 8, cudaMemcpyDeviceToHost, st), "download");
+            ddm::b200::check(cudaMemcpyAsync(baseline, d_out + B, B * 8, cudaMemcpyDeviceToHost, st), "download");
+            ddm::b200::check(cudaMemcpyAsync(tau, d_out + 2 * B, B * 8, cudaMemcpyDeviceToHost, st), "download");
+            ddm::b200::check(cudaMemcpyAsync(residual, d_out + 3 * B, B * 8, cudaMemcpyDeviceToHost, st), "download");
+            ddm::b200::check(cudaMemcpyAsync(flag, d_flag, B * 4, cudaMemcpyDeviceToHost, st), "download");
+            ddm::b200::check(cudaStreamSynchronize(st), "sync");
+            return 0;
+        });
+    });
+}
+
+int ddm_b200_estimate_diffusion(const double* tau, const int* flag, int64_t nbins, int64_t width,
+                                int64_t q_lo, int64_t q_hi, double* coefficient,
+                                int64_t* bins_used) {
+    return guarded([&] {
+        // `analysis.cpp:242-271`: least squares through the origin of 1/tau against q^2,
+        // q = 2 pi bin / width, over the ok fits of bins [q_lo, q_hi]
+        if (!tau || !flag || !coefficient || !bins_used) throw ddm::InputError("null buffer");
+        if (width < 1) throw ddm::InputError("estimate_diffusion: bad width");
+        const double two_pi = 2.0 * std::acos(-1.0);
+        double sxx = 0.0, sxy = 0.0;
+        int64_t used = 0;
+        for (int64_t b = std::max<int64_t>(q_lo, 0); b <= q_hi && b < nbins; ++b) {
+            if (flag[b] != 0) continue;
+            const double q = two_pi * double(b) / double(width);
+            const double x = q * q;
+            sxx += x * x;
+            sxy += x * (1.0 / tau[b]);
+            ++used;
+        }
+        *bins_used = used;
+        *coefficient = (used > 0 && sxx > 0.0) ? sxy / sxx : 0.0;
     });
 }
 

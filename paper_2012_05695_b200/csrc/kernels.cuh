@@ -114,6 +114,13 @@ cudaError_t launch_pairwise(const void* spec, int N, int64_t nq, const int* lags
                             double* out, int64_t out_stride, const int64_t* dest_of_slot,
                             int num_sms, cudaStream_t stream);
 
+// Relaxation fits, one warp per ring (`analysis.cpp:108-224`): means [n_lags][nbins] f64;
+// flag 0 ok, 1 degenerate, 2 no_converge, -1 not fitted.
+cudaError_t launch_fit_rings(const double* means, const int64_t* lags, int n_lags,
+                             const int64_t* counts, int64_t nbins, double dt, double* amp,
+                             double* base, double* tau, double* resid, int* flag,
+                             cudaStream_t stream);
+
 // Segmented sequences (SegTable over q_count sequences) -> the engine's tile-major layout T.
 template <typename S>
 cudaError_t launch_repack_segments(const void* recv, int64_t q_count, const SegTable& segs, int N,

@@ -377,6 +377,35 @@ def run_azimuthal_device(frames_ptr: int, pixel_bytes: int, width: int, height: 
     return nb.value, sp.value, tp.value, bool(fu.value)
 
 
+FIT_FLAGS = {0: "ok", 1: "degenerate", 2: "no_converge", -1: "not_fitted"}
+
+
+def fit_rings(means, lags, counts, frame_interval: float = 1.0, device: int = 0):
+    """ddm::fit_all_bins (`analysis.cpp:108-224`) on the device: per-ring
+    (amplitude, baseline, tau, residual, flag) arrays over the profile's bins."""
+    m = np.ascontiguousarray(means, dtype=np.float64)
+    lg = np.ascontiguousarray(lags, dtype=np.int64)
+    ct = np.ascontiguousarray(counts, dtype=np.int64)
+    nb = m.shape[1]
+    out = [np.zeros(nb) for _ in range(4)]
+    flag = np.zeros(nb, dtype=np.int32)
+    _check(lib().ddm_b200_fit_rings(_p(m, C.c_double), _p(lg, C.c_int64), C.c_int64(len(lg)),
+                                    _p(ct, C.c_int64), C.c_int64(nb), C.c_double(frame_interval),
+                                    device, *[_p(o, C.c_double) for o in out], _p(flag, C.c_int)))
+    return out[0], out[1], out[2], out[3], flag
+
+
+def estimate_diffusion(tau, flag, width: int, q_lo: int, q_hi: int):
+    """ddm::estimate_diffusion (`analysis.cpp:242-271`) -> (coefficient, bins_used)."""
+    t = np.ascontiguousarray(tau, dtype=np.float64)
+    f = np.ascontiguousarray(flag, dtype=np.int32)
+    coef, used = C.c_double(0.0), C.c_int64(0)
+    _check(lib().ddm_b200_estimate_diffusion(_p(t, C.c_double), _p(f, C.c_int), C.c_int64(len(t)),
+                                             C.c_int64(width), C.c_int64(q_lo), C.c_int64(q_hi),
+                                             C.byref(coef), C.byref(used)))
+    return coef.value, used.value
+
+
 def generate(width=64, height=64, frames=256, particles=100, diffusion=0.5, psf_sigma=1.0,
              amplitude=1000.0, background=100.0, frame_interval=1.0, seed=0) -> np.ndarray:
     """ddm::generate (`synth.cpp:98-132`), bit-identical frames [N, H, W] uint16."""

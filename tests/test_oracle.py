@@ -160,3 +160,25 @@ def test_pairwise_goldens_pin_the_oracle():
         assert O.relative_deviation(g[f"direct_{key}"], ref) <= 1e-9
         pairs = sum(n - m for m in O.normalize_lags(lags, n) if m > 0)
         assert g[f"direct_counters_{key}"][2] == pairs
+
+
+def test_fit_restatement_recovers_a_known_relaxation():
+    t = np.arange(1, 200, dtype=np.float64) * 0.5
+    y = 3.0 * (1.0 - np.exp(-t / 7.5)) + 0.25
+    a, b, tau, res, flag = O.fit_exponential(t, y)
+    assert flag == "ok" and abs(tau - 7.5) < 1e-6 and abs(a - 3.0) < 1e-6 and abs(b - 0.25) < 1e-6
+    assert O.fit_exponential(t, np.full_like(t, 2.0))[4] == "degenerate"
+    d, used = O.estimate_diffusion({2: (1, 0, 1 / (0.3 * (2 * np.pi * 2 / 64) ** 2), 0, "ok"),
+                                    3: (1, 0, 1 / (0.3 * (2 * np.pi * 3 / 64) ** 2), 0, "ok")}, 64, 2, 10)
+    assert used == 2 and abs(d - 0.3) < 1e-12
+
+
+def test_estimate_diffusion_through_the_abi():
+    """Host-only C-ABI entry (no device): the same least squares as the oracle."""
+    from paper_2012_05695_b200 import ddm
+    if not ddm.LIB_PATH.exists():
+        pytest.skip("library not built")
+    taus = np.array([0, 0, 1 / (0.3 * (2 * np.pi * 2 / 64) ** 2), 5.0, 1 / (0.3 * (2 * np.pi * 4 / 64) ** 2)])
+    flags = np.array([-1, 0, 0, 2, 0], dtype=np.int32)
+    d, used = ddm.estimate_diffusion(taus, flags, 64, 2, 10)
+    assert used == 2 and abs(d - 0.3) < 1e-12
