@@ -96,6 +96,15 @@ int ddm_b200_run_raw_stack(const char* path, const ddm_b200_run_config* config,
                            int64_t* out_n_lags, ddm_b200_counters* counters,
                            ddm_b200_timing* timing);
 
+/* ddm::run over PgmDirSource (frame_source.cpp:80-95): a directory of P5 / maxval 65535
+   frames, sorted by file name.  Frames are read by a thread pool into pinned staging and
+   streamed to HBM (as for raw stacks). */
+int ddm_b200_run_pgm_dir(const char* dir, const ddm_b200_run_config* config, double* out_values,
+                         int64_t out_capacity, int64_t* out_lags, int64_t* out_n_lags,
+                         ddm_b200_counters* counters, ddm_b200_timing* timing);
+/* Dimensions of a stack on disk (format 0 raw_stack, 1 pgm_dir; open_frame_source). */
+int ddm_b200_stack_dims(const char* path, int format, int* width, int* height, int* frames);
+
 /* Device-resident WITH_FT: frames already in HBM (pixel_bytes 2 = u16, 1 = u8), map written
    to HBM as lag-major [n_lags][height*(width/2+1)] f32 (out_f64 = 0) or f64.  Positions
    outside a cutoff are left untouched.  Runs on the library's stream for `device`, ordered

@@ -146,8 +146,21 @@ Engine::Engine(int device) : device_(device) {
     for (auto& e : ev_) check(cudaEventCreate(&e), "cudaEventCreate");
 }
 
+void* Engine::pinned(int slot, size_t bytes) {
+    if (pinned_bytes_[slot] < bytes) {
+        if (pinned_[slot]) cudaFreeHost(pinned_[slot]);
+        pinned_[slot] = nullptr;
+        pinned_bytes_[slot] = 0;
+        check(cudaMallocHost(&pinned_[slot], bytes), "cudaMallocHost");
+        pinned_bytes_[slot] = bytes;
+    }
+    return pinned_[slot];
+}
+
 Engine::~Engine() {
     cudaSetDevice(device_);
+    for (auto p : pinned_)
+        if (p) cudaFreeHost(p);
     for (auto e : timing_events_) cudaEventDestroy(e);
     for (auto e : chunk_events_) cudaEventDestroy(e);
     if (cols_stream_) cudaStreamDestroy(cols_stream_);

@@ -141,6 +141,9 @@ public:
     // (spec.d_out, spec.out_stride, identity or flat positions). Single group.
     void run_pairwise(const RunSpec& spec, PhaseTimes* times = nullptr);
 
+    // Pinned host staging buffer `slot` (0 or 1) of at least `bytes`, kept across runs.
+    void* pinned(int slot, size_t bytes);
+
     // Device staging buffer for frames owned by the engine.
     void* frame_buffer(size_t bytes) { return frames_.ensure(bytes); }
     void* scratch(size_t bytes) { return user_scratch_.ensure(bytes); }
@@ -179,6 +182,8 @@ private:
     std::vector<cudaEvent_t> timing_events_;   // reusable phase-timing events
     std::vector<cudaEvent_t> chunk_events_;    // row/column pass ordering across streams
     cudaStream_t cols_stream_ = nullptr;       // column passes (overlapped spatial step)
+    void* pinned_[2] = {nullptr, nullptr};
+    size_t pinned_bytes_[2] = {0, 0};
     std::mutex mu_;
     // last ring plan and its device copy (geometry only, reused across runs)
     struct RingCache {

@@ -207,6 +207,28 @@ int ddm_b200_run_raw_stack(const char* path, const ddm_b200_run_config* config, 
     });
 }
 
+int ddm_b200_run_pgm_dir(const char* dir, const ddm_b200_run_config* config, double* out_values,
+                         int64_t out_capacity, int64_t* out_lags, int64_t* out_n_lags,
+                         ddm_b200_counters* counters, ddm_b200_timing* timing) {
+    return guarded([&] {
+        if (!dir) throw ddm::InputError("null path");
+        ddm::PgmDirSource src(dir);
+        const auto a = ddm::run_into(src, to_config(config), out_values, out_capacity);
+        emit(a, out_lags, out_n_lags, counters, timing);
+    });
+}
+
+int ddm_b200_stack_dims(const char* path, int format, int* width, int* height, int* frames) {
+    return guarded([&] {
+        if (!path || !width || !height || !frames) throw ddm::InputError("null argument");
+        const auto src = ddm::open_frame_source(path, format == 1 ? ddm::StackFormat::PgmDir
+                                                                  : ddm::StackFormat::RawStack);
+        *width = src->width();
+        *height = src->height();
+        *frames = src->frames();
+    });
+}
+
 int ddm_b200_run_device(const void* d_frames, int pixel_bytes, int width, int height, int frames,
                         int precision, const int64_t* lags, int64_t n_lags, int has_q_max,
                         double q_max, void* d_out, int out_f64, int device, void* stream,

@@ -18,7 +18,10 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
+#include <exception>
+#include <thread>
 
 #include <unistd.h>
 
@@ -66,43 +69,62 @@ const void* stage_frames(b200::Engine& eng, const detail::Ingest& in, double& di
                                     cudaMemcpyHostToDevice, st), "frame upload");
         b200::check(cudaStreamSynchronize(st), "sync");
     } else {
+        // FrameSource::read_frame is thread-safe (`frame_source.hpp:16-17`): frames of a
+        // 32 MiB chunk are read by a pool of threads into pinned staging, the chunk's DMA to
+        // HBM runs while the next chunk is read (two pinned buffers, cached by the engine)
         const int chunk = int(std::max<std::size_t>(1, std::min<std::size_t>(
                                   std::size_t(in.frames), (32u << 20) / (ppf * 2))));
-        std::uint16_t* pinned[2] = {nullptr, nullptr};
+        std::uint16_t* pinned[2] = {
+            static_cast<std::uint16_t*>(eng.pinned(0, ppf * 2 * std::size_t(chunk))),
+            static_cast<std::uint16_t*>(eng.pinned(1, ppf * 2 * std::size_t(chunk)))};
         cudaEvent_t done[2];
-        for (int i = 0; i < 2; ++i) {
-            b200::check(cudaMallocHost(reinterpret_cast<void**>(&pinned[i]), ppf * 2 * chunk),
-                        "cudaMallocHost");
-            b200::check(cudaEventCreate(&done[i]), "cudaEventCreate");
-        }
+        for (int i = 0; i < 2; ++i) b200::check(cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming), "cudaEventCreate");
+        struct Events {
+            cudaEvent_t* e;
+            ~Events() { cudaEventDestroy(e[0]); cudaEventDestroy(e[1]); }
+        } ev_guard{done};
+        const int nthreads = int(std::max(1u, std::min(8u, std::thread::hardware_concurrency())));
         int slot = 0;
         bool used[2] = {false, false};
-        try {
-            for (int f0 = 0; f0 < in.frames; f0 += chunk) {
-                const int nf = std::min(chunk, in.frames - f0);
-                if (used[slot]) b200::check(cudaEventSynchronize(done[slot]), "sync");
-                for (int i = 0; i < nf; ++i)
-                    in.source->read_frame(f0 + i, {pinned[slot] + std::size_t(i) * ppf, ppf});
-                b200::check(cudaMemcpyAsync(static_cast<std::uint16_t*>(d) + std::size_t(f0) * ppf,
-                                            pinned[slot], ppf * 2 * nf, cudaMemcpyHostToDevice, st),
-                            "frame upload");
-                b200::check(cudaEventRecord(done[slot], st), "cudaEventRecord");
-                used[slot] = true;
-                slot ^= 1;
+        for (int f0 = 0; f0 < in.frames; f0 += chunk) {
+            const int nf = std::min(chunk, in.frames - f0);
+            if (used[slot]) b200::check(cudaEventSynchronize(done[slot]), "sync");
+            std::uint16_t* buf = pinned[slot];
+            std::atomic<int> next{0};
+            std::exception_ptr failure;
+            std::mutex failure_mu;
+            // raw stacks: each worker takes a contiguous run of frames as one positioned read
+            const auto* raw = dynamic_cast<const RawStackFileSource*>(in.source);
+            static const bool per_frame = std::getenv("DDM_INGEST_PER_FRAME") != nullptr;
+            const int run = (raw && !per_frame) ? std::max(1, (nf + nthreads - 1) / nthreads) : 1;
+            auto work = [&] {
+                for (int i = next.fetch_add(run); i < nf; i = next.fetch_add(run)) {
+                    try {
+                        const int cnt = std::min(run, nf - i);
+                        if (raw) raw->read_frames(f0 + i, cnt, buf + std::size_t(i) * ppf);
+                        else in.source->read_frame(f0 + i, {buf + std::size_t(i) * ppf, ppf});
+                    } catch (...) {
+                        std::lock_guard<std::mutex> lk(failure_mu);
+                        if (!failure) failure = std::current_exception();
+                        next = nf;
+                    }
+                }
+            };
+            std::vector<std::thread> pool;
+            for (int t = 1; t < std::min(nthreads, nf); ++t) pool.emplace_back(work);
+            work();
+            for (auto& t : pool) t.join();
+            if (failure) {
+                cudaStreamSynchronize(st);
+                std::rethrow_exception(failure);
             }
-            b200::check(cudaStreamSynchronize(st), "sync");
-        } catch (...) {
-            cudaStreamSynchronize(st);
-            for (int i = 0; i < 2; ++i) {
-                cudaFreeHost(pinned[i]);
-                cudaEventDestroy(done[i]);
-            }
-            throw;
+            b200::check(cudaMemcpyAsync(static_cast<std::uint16_t*>(d) + std::size_t(f0) * ppf, buf,
+                                        ppf * 2 * nf, cudaMemcpyHostToDevice, st), "frame upload");
+            b200::check(cudaEventRecord(done[slot], st), "cudaEventRecord");
+            used[slot] = true;
+            slot ^= 1;
         }
-        for (int i = 0; i < 2; ++i) {
-            cudaFreeHost(pinned[i]);
-            cudaEventDestroy(done[i]);
-        }
+        b200::check(cudaStreamSynchronize(st), "sync");
     }
     disk_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     return d;

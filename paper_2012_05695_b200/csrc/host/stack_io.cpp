@@ -5,8 +5,13 @@
 #include "ddm/image_stack.hpp"
 #include "json_lite.hpp"
 
+#include <algorithm>
+#include <cctype>
 #include <cstring>
 #include <fstream>
+
+#include <fcntl.h>
+#include <unistd.h>
 
 namespace fs = std::filesystem;
 
@@ -63,8 +68,16 @@ RawHeader read_raw_header(std::ifstream& in, const fs::path& path) {
 }  // namespace
 
 ImageStack load_stack(const fs::path& path, StackFormat format) {
-    if (format != StackFormat::RawStack)
-        throw InputError("pgm_dir stacks are not supported by the b200 build; convert to raw_stack");
+    if (format == StackFormat::PgmDir) {
+        const PgmDirSource src(path);
+        ImageStack st;
+        st.width = src.width();
+        st.height = src.height();
+        st.frames = src.frames();
+        st.pixels.resize(std::size_t(st.width) * st.height * st.frames);
+        for (int n = 0; n < st.frames; ++n) src.read_frame(n, st.frame(n));
+        return st;
+    }
     if (!fs::exists(path)) throw IoError("path does not exist: " + path.string());
     std::ifstream in(path, std::ios::binary);
     if (!in) throw IoError("cannot open " + path.string());
@@ -127,28 +140,36 @@ void ViewFrameSource::read_frame(int n, std::span<std::uint16_t> out) const {
 
 RawStackFileSource::RawStackFileSource(const fs::path& path) : path_(path) {
     if (!fs::exists(path)) throw IoError("path does not exist: " + path.string());
-    file_.open(path, std::ios::binary);
-    if (!file_) throw IoError("cannot open " + path.string());
-    const RawHeader h = read_raw_header(file_, path);
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw IoError("cannot open " + path.string());
+    const RawHeader h = read_raw_header(in, path);
     width_ = h.width;
     height_ = h.height;
     frames_ = h.frames;
     frame_interval_ = h.frame_interval;
     payload_offset_ = h.payload_offset;
-    file_.seekg(0, std::ios::end);
-    const std::int64_t size = std::int64_t(file_.tellg());
+    const std::int64_t size = std::int64_t(fs::file_size(path));
     if (size < payload_offset_ + 2 * pixels_per_frame() * frames_)
         throw InputError("raw_stack " + path.string() + ": truncated payload");
+    fd_ = ::open(path.c_str(), O_RDONLY | O_CLOEXEC);
+    if (fd_ < 0) throw IoError("cannot open " + path.string());
+}
+
+RawStackFileSource::~RawStackFileSource() {
+    if (fd_ >= 0) ::close(fd_);
 }
 
 void RawStackFileSource::read_frames(int first, int count, std::uint16_t* out) const {
+    // one positioned read: no shared file offset, so concurrent calls need no lock (the
+    // reference serialises seek + read behind a mutex, `frame_source.cpp:64-78`)
     const std::int64_t bytes = 2 * pixels_per_frame() * count;
-    {
-        std::lock_guard<std::mutex> lock(mutex_);
-        file_.clear();
-        file_.seekg(payload_offset_ + std::int64_t(first) * 2 * pixels_per_frame());
-        file_.read(reinterpret_cast<char*>(out), bytes);
-        if (file_.gcount() != bytes) throw IoError("raw_stack " + path_.string() + ": short read");
+    std::int64_t done = 0;
+    auto* dst = reinterpret_cast<char*>(out);
+    while (done < bytes) {
+        const ssize_t r = ::pread(fd_, dst + done, std::size_t(bytes - done),
+                                  off_t(payload_offset_ + std::int64_t(first) * 2 * pixels_per_frame() + done));
+        if (r <= 0) throw IoError("raw_stack " + path_.string() + ": short read");
+        done += r;
     }
     // payload is little endian; this build targets little-endian hosts (as the reference)
 }
@@ -157,9 +178,85 @@ void RawStackFileSource::read_frame(int n, std::span<std::uint16_t> out) const {
     read_frames(n, 1, out.data());
 }
 
+namespace {
+
+// PGM header token: whitespace and '#' comments skipped (`image_stack.cpp:20-39`)
+std::string pgm_token(std::istream& in) {
+    int c = in.get();
+    while (c != EOF) {
+        if (c == '#') {
+            while (c != EOF && c != '\n') c = in.get();
+        } else if (!std::isspace(c)) {
+            break;
+        }
+        c = in.get();
+    }
+    std::string tok;
+    while (c != EOF && !std::isspace(c)) {
+        tok.push_back(char(c));
+        c = in.get();
+    }
+    return tok;
+}
+
+int pgm_int(const std::string& tok, const char* what, const fs::path& f) {
+    std::size_t pos = 0;
+    long v = 0;
+    try {
+        v = std::stol(tok, &pos);
+    } catch (const std::exception&) {
+        pos = 0;
+    }
+    if (pos != tok.size() || tok.empty() || v < 1)
+        throw InputError("pgm " + f.string() + ": bad " + what + " '" + tok + "'");
+    return int(v);
+}
+
+// reads one P5 / maxval 65535 frame (big-endian samples) into out (or only the size)
+void read_pgm(const fs::path& f, int& w, int& h, std::uint16_t* out, std::size_t capacity) {
+    std::ifstream in(f, std::ios::binary);
+    if (!in) throw IoError("cannot open " + f.string());
+    const std::string magic = pgm_token(in);
+    if (magic != "P5") throw InputError("pgm " + f.string() + ": not a binary PGM (magic '" + magic + "')");
+    w = pgm_int(pgm_token(in), "width", f);
+    h = pgm_int(pgm_token(in), "height", f);
+    const std::string maxval = pgm_token(in);
+    if (maxval != "65535") throw InputError("pgm " + f.string() + ": maxval must be 65535, got '" + maxval + "'");
+    if (!out) return;
+    const std::size_t count = std::size_t(w) * std::size_t(h);
+    if (count > capacity) throw InputError("pgm " + f.string() + ": frame dimensions differ from the first frame");
+    in.read(reinterpret_cast<char*>(out), std::streamsize(count * 2));
+    if (std::size_t(in.gcount()) != count * 2) throw InputError("pgm " + f.string() + ": truncated payload");
+    for (std::size_t i = 0; i < count; ++i) out[i] = std::uint16_t((out[i] >> 8) | (out[i] << 8));
+}
+
+std::vector<fs::path> pgm_files(const fs::path& dir) {
+    if (!fs::exists(dir)) throw IoError("path does not exist: " + dir.string());
+    if (!fs::is_directory(dir)) throw InputError("pgm_dir input is not a directory: " + dir.string());
+    std::vector<fs::path> files;
+    for (const auto& e : fs::directory_iterator(dir))
+        if (e.is_regular_file() && e.path().extension() == ".pgm") files.push_back(e.path());
+    if (files.empty()) throw InputError("no *.pgm files in " + dir.string());
+    std::sort(files.begin(), files.end(),
+              [](const fs::path& a, const fs::path& b) { return a.filename().string() < b.filename().string(); });
+    return files;
+}
+
+}  // namespace
+
+PgmDirSource::PgmDirSource(const fs::path& dir) : files_(pgm_files(dir)) {
+    read_pgm(files_.front(), width_, height_, nullptr, 0);
+}
+
+void PgmDirSource::read_frame(int n, std::span<std::uint16_t> out) const {
+    int w = 0, h = 0;
+    read_pgm(files_[std::size_t(n)], w, h, out.data(), out.size());
+    if (w != width_ || h != height_)
+        throw InputError("pgm " + files_[std::size_t(n)].string() + ": frame dimensions differ from the first frame");
+}
+
 std::unique_ptr<FrameSource> open_frame_source(const fs::path& path, StackFormat format) {
-    if (format == StackFormat::PgmDir)
-        throw InputError("pgm_dir stacks are not supported by the b200 build; convert to raw_stack");
+    if (format == StackFormat::PgmDir) return std::make_unique<PgmDirSource>(path);
     return std::make_unique<RawStackFileSource>(path);
 }
 

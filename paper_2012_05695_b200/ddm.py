@@ -266,6 +266,31 @@ def run_raw_stack(path: str, config: RunConfig) -> ResultArchive:
                          {f: float(getattr(timing, f)) for f, _ in Timing._fields_})
 
 
+def run_pgm_dir(path: str, config: RunConfig) -> ResultArchive:
+    """ddm::run over a PgmDirSource (`frame_source.cpp:80-95`)."""
+    w, h, n = C.c_int(0), C.c_int(0), C.c_int(0)
+    _check(lib().ddm_b200_stack_dims(str(path).encode(), 1, C.byref(w), C.byref(h), C.byref(n)))
+    w, h, n = w.value, h.value, n.value
+    n_out = len(config.lags) if len(config.lags) else n
+    plane = h * half_cols(w)
+    values = np.empty(max(n_out, 1) * plane)
+    out_lags = np.zeros(max(n_out, 1), dtype=np.int64)
+    n_lags = C.c_int64(0)
+    counters, timing = Counters(), Timing()
+    keep: list = []
+    c = _config(config, keep)
+    _check(lib().ddm_b200_run_pgm_dir(str(path).encode(), C.byref(c), _p(values, C.c_double),
+                                      C.c_int64(values.size), _p(out_lags, C.c_int64),
+                                      C.byref(n_lags), C.byref(counters), C.byref(timing)))
+    k = n_lags.value
+    return ResultArchive(values[: k * plane].reshape(k, h, half_cols(w)), out_lags[:k].copy(), w, h,
+                         n, 1.0, config.algorithm,
+                         "f64" if config.algorithm == "direct" else config.precision, config.q_max,
+                         config.workers,
+                         {f: int(getattr(counters, f)) for f, _ in Counters._fields_},
+                         {f: float(getattr(timing, f)) for f, _ in Timing._fields_})
+
+
 @dataclass
 class LagProfile:
     d: np.ndarray
