@@ -175,6 +175,15 @@ def cpu_baseline_sample():
                       f"phases {json.dumps({k: round(v, 3) for k, v in r.timing.items()})}"}
 
 
+def shard_chunks(n: int) -> int:
+    """Frame chunks of the register spatial path for an n-frame shard at 512^2
+    (Engine::spatial_pass: half the frames per chunk, rounded down to 16-frame groups)."""
+    fc = 16
+    f = max(fc, (n + 1) // 2 - ((n + 1) // 2) % fc)
+    f = min(n, f)
+    return -(-n // f)
+
+
 def sharded_arm(args, rank: int, world: int):
     """N > 1: the sharded pass (spatial shard -> NCCL all-to-all -> temporal slice)."""
     import torch
@@ -299,8 +308,9 @@ def sharded_arm(args, rank: int, world: int):
                     "h2d_bytes_per_step": int(st.nbytes),
                     "d2h_bytes_per_step": int(4 * N * Q), "ms_per_step": e2e_s * 1e3,
                     "path": "per rank: pinned frame shard H2D, sharded pass, f32 partial D2H"},
-            # per step: row + column pass per 32-frame chunk of the shard, one temporal launch
-            "gpu_launches": args.steps * (2 * (-(-n_r // 32)) + 1),
+            # per step: a row and a column pass per frame chunk of the shard (two chunks of
+            # whole 16-frame column groups, Engine::spatial_pass) and one temporal launch
+            "gpu_launches": args.steps * (2 * shard_chunks(n_r) + 1),
         }
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
