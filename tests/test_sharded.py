@@ -121,6 +121,7 @@ def _gloo_worker(rank, world, port, W, H, N, precision, lags, result_path):
     (2, 16, 12, 20, "f64", None),
     (3, 10, 8, 17, "f64", [0, 1, 3, 16]),   # odd N: odd tail segment
     (2, 32, 32, 64, "f32", None),
+    (4, 12, 10, 23, "f64", [0, 2, 22]),     # four ranks, odd N, uneven wave-vector slices
 ])
 def test_gloo_sharded_matches_single_process(tmp_path, world, W, H, N, precision, lags):
     import torch.multiprocessing as mp
