@@ -105,6 +105,10 @@ int ddm_b200_run_pgm_dir(const char* dir, const ddm_b200_run_config* config, dou
 /* Dimensions of a stack on disk (format 0 raw_stack, 1 pgm_dir; open_frame_source). */
 int ddm_b200_stack_dims(const char* path, int format, int* width, int* height, int* frames);
 
+/* ddm::load_stack (image_stack.cpp:160-247): the whole stack into out (frame-major u16,
+   capacity in samples); host only. */
+int ddm_b200_load_stack(const char* path, int format, uint16_t* out, int64_t capacity);
+
 /* Device-resident WITH_FT: frames already in HBM (pixel_bytes 2 = u16, 1 = u8), map written
    to HBM as lag-major [n_lags][height*(width/2+1)] f32 (out_f64 = 0) or f64.  Positions
    outside a cutoff are left untouched.  Runs on the library's stream for `device`, ordered

@@ -229,6 +229,15 @@ int ddm_b200_stack_dims(const char* path, int format, int* width, int* height, i
     });
 }
 
+int ddm_b200_load_stack(const char* path, int format, uint16_t* out, int64_t capacity) {
+    return guarded([&] {
+        if (!path || !out) throw ddm::InputError("null argument");
+        const auto st = ddm::load_stack(path, format == 1 ? ddm::StackFormat::PgmDir : ddm::StackFormat::RawStack);
+        if (int64_t(st.pixels.size()) > capacity) throw ddm::InputError("output capacity too small");
+        std::copy(st.pixels.begin(), st.pixels.end(), out);
+    });
+}
+
 int ddm_b200_run_device(const void* d_frames, int pixel_bytes, int width, int height, int frames,
                         int precision, const int64_t* lags, int64_t n_lags, int has_q_max,
                         double q_max, void* d_out, int out_f64, int device, void* stream,

@@ -266,6 +266,18 @@ def run_raw_stack(path: str, config: RunConfig) -> ResultArchive:
                          {f: float(getattr(timing, f)) for f, _ in Timing._fields_})
 
 
+def load_stack(path: str, fmt: str = "raw_stack") -> np.ndarray:
+    """ddm::load_stack (raw_stack | pgm_dir) -> [N, H, W] uint16 (host only)."""
+    f = {"raw_stack": 0, "pgm_dir": 1}.get(fmt)
+    if f is None:
+        raise InputError(f"unknown stack format '{fmt}'")
+    w, h, n = C.c_int(0), C.c_int(0), C.c_int(0)
+    _check(lib().ddm_b200_stack_dims(str(path).encode(), f, C.byref(w), C.byref(h), C.byref(n)))
+    out = np.empty((n.value, h.value, w.value), dtype=np.uint16)
+    _check(lib().ddm_b200_load_stack(str(path).encode(), f, _p(out, C.c_uint16), C.c_int64(out.size)))
+    return out
+
+
 def run_pgm_dir(path: str, config: RunConfig) -> ResultArchive:
     """ddm::run over a PgmDirSource (`frame_source.cpp:80-95`)."""
     w, h, n = C.c_int(0), C.c_int(0), C.c_int(0)
