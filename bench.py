@@ -332,28 +332,34 @@ def our_arm(args, rank: int, world: int):
     out_d = torch.empty(N * plane, dtype=torch.float32, device=f"cuda:{dev}")
     stream = torch.cuda.current_stream()
 
-    def step():
+    def step(timing=False):
         return ddm.run_device(frames_d.data_ptr(), 2, W, H, N, out_d.data_ptr(), "f32",
-                              out_f64=False, device=dev, stream=stream.cuda_stream)
+                              out_f64=False, device=dev, stream=stream.cuda_stream, timing=timing)
 
     for _ in range(max(args.warmup, 3)):
         step()
     torch.cuda.synchronize()
+    # stage breakdown and launch count (per-step device times need a host sync, so they are
+    # taken outside the timed region)
+    sp_ms, tp_ms, per_step = [], [], 0
+    for _ in range(3):
+        s, t, nl = step(timing=True)
+        sp_ms.append(s)
+        tp_ms.append(t)
+        per_step = nl
+    torch.cuda.synchronize()
 
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    sp_ms, tp_ms, launches = [], [], 0
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(dev) as clk:
         e0.record(stream)
         for _ in range(args.steps):
-            s, t, nl = step()
-            sp_ms.append(s)
-            tp_ms.append(t)
-            launches += nl
+            step()       # asynchronous: steps queue back to back on the stream
         e1.record(stream)
         torch.cuda.synchronize()
+    launches = per_step * args.steps
     if dist:
         dist.barrier()
     ms_total = e0.elapsed_time(e1)

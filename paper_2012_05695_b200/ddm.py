@@ -457,11 +457,21 @@ def generate(width=64, height=64, frames=256, particles=100, diffusion=0.5, psf_
 
 def run_device(frames_ptr: int, pixel_bytes: int, width: int, height: int, frames: int,
                out_ptr: int, precision: str = "f32", out_f64: bool = False, lags=None,
-               q_max: Optional[float] = None, device: int = 0, stream: int = 0):
+               q_max: Optional[float] = None, device: int = 0, stream: int = 0,
+               timing: bool = True):
     """Device-resident WITH_FT (frames and map already in HBM, e.g. torch tensors' data_ptr).
-    Returns (spatial_ms, temporal_ms, kernel_launches) of device time."""
+    Returns (spatial_ms, temporal_ms, kernel_launches) of device time; timing=False keeps the
+    call fully asynchronous (no host synchronisation) and returns zeros."""
     lag_arr = np.ascontiguousarray(np.asarray(lags if lags is not None else [], dtype=np.int64))
     sp, tp, nl = C.c_double(0), C.c_double(0), C.c_int(0)
+    if not timing:
+        _check(lib().ddm_b200_run_device(
+            C.c_void_p(frames_ptr), pixel_bytes, width, height, frames,
+            0 if precision == "f32" else 1, _p(lag_arr, C.c_int64) if len(lag_arr) else None,
+            C.c_int64(len(lag_arr)), 0 if q_max is None else 1,
+            C.c_double(0.0 if q_max is None else q_max), C.c_void_p(out_ptr), 1 if out_f64 else 0,
+            device, C.c_void_p(stream), None, None, None))
+        return 0.0, 0.0, 0
     _check(lib().ddm_b200_run_device(
         C.c_void_p(frames_ptr), pixel_bytes, width, height, frames,
         0 if precision == "f32" else 1, _p(lag_arr, C.c_int64) if len(lag_arr) else None,
