@@ -378,6 +378,9 @@ __global__ void transpose_lags_kernel(const float* __restrict__ out_q, int N, in
 
 }  // namespace
 
+cudaError_t launch_long2(const TemporalArgs& a, int64_t q0, int64_t q1, float* out_q, int num_sms,
+                         cudaStream_t stream);
+
 bool temporal_long_supported(int N, int N2, int scalar_bytes) {
     return scalar_bytes == 4 && (N2 == 4096 || N2 == 8192) && N > N2 / 4 && N <= N2 / 2 && N % 2 == 0;
 }
@@ -392,7 +395,10 @@ cudaError_t launch_temporal_long(const TemporalArgs& a, int num_sms, void* out_q
     if (reinterpret_cast<uintptr_t>(a.spec) % 16 != 0) return cudaErrorMisalignedAddress;
     if (!temporal_warp_segments_ok(a.segs, a.N)) return cudaErrorInvalidValue;
     const int R = a.N2 / kF;
+    // the balanced two-group engine (temporal_long2.cu) unless DDM_LONG_V1 asks for this one
+    static const bool v1 = std::getenv("DDM_LONG_V1") != nullptr;
     auto launch = [&](int64_t q0, int64_t q1) {
+        if (!v1) return launch_long2(a, q0, q1, static_cast<float*>(out_q), num_sms, stream);
         return R == 4 ? launch_long<4>(a, q0, q1, static_cast<float*>(out_q), num_sms, stream)
                       : launch_long<8>(a, q0, q1, static_cast<float*>(out_q), num_sms, stream);
     };
