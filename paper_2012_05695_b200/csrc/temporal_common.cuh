@@ -46,6 +46,21 @@ __device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t b
         : "memory");
 }
 
+// wait with backoff: a warp whose copy has not landed sleeps between polls instead of
+// taking issue slots from the warps that have work
+__device__ __forceinline__ void mbar_wait_backoff(unsigned long long* bar, uint32_t phase) {
+    uint32_t ok = 0;
+    while (true) {
+        asm volatile(
+            "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}"
+            : "=r"(ok)
+            : "r"(smem_addr(bar)), "r"(phase)
+            : "memory");
+        if (ok) return;
+        __nanosleep(64);
+    }
+}
+
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t phase) {
     asm volatile(
         "{\n.reg .pred p;\nWAIT_%=:\n"

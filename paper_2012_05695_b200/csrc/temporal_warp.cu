@@ -32,6 +32,7 @@ namespace {
 
 using namespace tc;
 
+constexpr bool kBackoff = true;       // sleep between polls of the sequence copy
 constexpr int kL = 1024;              // half padded length
 constexpr int kN2 = 2048;
 constexpr int kPad = kL + kL / 32;    // slots per buffer (FFT scratch pitch 33 x 32)
@@ -117,7 +118,8 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
     // (to start the next copy), emit(m, d(m)) for every m < N.
     auto process = [&](int64_t q, bool live, auto&& after_reload, auto&& emit) {
         if (live) {
-            mbar_wait(&my.bar, phase);
+            if (kBackoff) mbar_wait_backoff(&my.bar, phase);
+            else mbar_wait(&my.bar, phase);
             phase ^= 1u;
         }
 
