@@ -98,6 +98,11 @@ ResultArchive run_into(FrameSource& source, const RunConfig& config, double* out
 
 ResultMap merge_partials(const std::vector<std::filesystem::path>& files);
 
+/// What `ddm analyze` writes (`tools/ddm_cli.cpp:206-240`), as a library call: run with the
+/// workspace in `out_dir`, write_results (d_m<lag>.bin + index.json), the ring average
+/// (radial.csv) and the ring fits (fits.csv). The CLI's own run.json echo is not written.
+ResultArchive analyze(FrameSource& source, RunConfig config, const std::filesystem::path& out_dir);
+
 } // namespace ddm
 
 #endif

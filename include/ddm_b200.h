@@ -102,6 +102,15 @@ int ddm_b200_run_raw_stack(const char* path, const ddm_b200_run_config* config,
 int ddm_b200_run_pgm_dir(const char* dir, const ddm_b200_run_config* config, double* out_values,
                          int64_t out_capacity, int64_t* out_lags, int64_t* out_n_lags,
                          ddm_b200_counters* counters, ddm_b200_timing* timing);
+/* `ddm analyze` (tools/ddm_cli.cpp:206-240) as one call: open the stack (format 0 raw_stack,
+   1 pgm_dir, -1 auto = directory -> pgm_dir), ddm::run with the workspace in out_dir,
+   write_results (d_m<lag>.bin + index.json), radial.csv (azimuthal_average +
+   write_radial_csv) and, when at least 4 lags >= 1 exist, fits.csv (fit_all_bins +
+   write_fits_csv).  The CLI's run.json option echo is left to the caller (the Python
+   wrapper writes it).  fits_written = 1 if fits.csv was written. */
+int ddm_b200_analyze(const char* path, int format, const ddm_b200_run_config* config,
+                     const char* out_dir, int64_t* out_n_lags, int64_t* fits_written,
+                     ddm_b200_counters* counters, ddm_b200_timing* timing);
 /* Dimensions of a stack on disk (format 0 raw_stack, 1 pgm_dir; open_frame_source). */
 int ddm_b200_stack_dims(const char* path, int format, int* width, int* height, int* frames);
 

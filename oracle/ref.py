@@ -224,3 +224,20 @@ def host_cores() -> int:
         return len(os.sched_getaffinity(0))
     except AttributeError:  # pragma: no cover
         return os.cpu_count() or 1
+
+
+def analyze(path: str, out_dir: str, fmt: str = "raw_stack", algorithm: str = "with_ft",
+            precision: str = "f64", lags=(), q_max=None, memory_bytes: int = 1 << 40,
+            workers: int = 2) -> None:
+    """The `ddm analyze` artefacts (`proj/tools/ddm_cli.cpp:206-240` composition): d_m*.bin,
+    index.json, radial.csv and fits.csv written by the reference library into out_dir."""
+    lag_arr = np.ascontiguousarray(np.asarray(lags, dtype=np.int64))
+    err = C.create_string_buffer(1024)
+    rc = lib().ref_analyze(str(path).encode(), 1 if fmt == "pgm_dir" else 0,
+                           {"with_ft": 0, "without_ft": 1, "direct": 2}[algorithm],
+                           0 if precision == "f32" else 1,
+                           _p(lag_arr, C.c_int64) if len(lag_arr) else None,
+                           C.c_int64(len(lag_arr)), 0 if q_max is None else 1,
+                           C.c_double(0.0 if q_max is None else q_max), C.c_int64(memory_bytes),
+                           workers, str(out_dir).encode(), err, 1024)
+    _check(rc, err)

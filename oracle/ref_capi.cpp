@@ -8,6 +8,7 @@
 // 0 ok, 1 InputError, 2 PlanError/bad_alloc, 3 IoError, 5 other.
 
 #include <ddm/analysis.hpp>
+#include <ddm/archive.hpp>
 #include <ddm/errors.hpp>
 #include <ddm/frame_source.hpp>
 #include <ddm/scheduler.hpp>
@@ -19,6 +20,7 @@
 #include <complex>
 #include <cstdint>
 #include <cstring>
+#include <filesystem>
 #include <new>
 #include <string>
 #include <vector>
@@ -263,6 +265,44 @@ int ref_azimuthal(const double* values, const std::int64_t* lags, std::int64_t n
             throw ddm::InputError("ref_azimuthal: bin capacity too small");
         std::copy(prof.counts.begin(), prof.counts.end(), counts);
         std::copy(prof.means.begin(), prof.means.end(), means);
+    });
+}
+
+} // extern "C"
+
+extern "C" {
+
+// The `ddm analyze` artefact set, composed exactly as tools/ddm_cli.cpp:206-240 composes it
+// (open_frame_source, run with out_dir, write_results, azimuthal_average + write_radial_csv,
+// fit_all_bins + write_fits_csv); run.json is the CLI's option echo and is not written.
+// format: 0 raw_stack, 1 pgm_dir.
+int ref_analyze(const char* path, int format, int algorithm, int precision,
+                const std::int64_t* lags, std::int64_t n_lags, int has_q_max, double q_max,
+                std::int64_t memory_bytes, int workers, const char* out_dir, char* err,
+                int errlen) {
+    return guarded(err, errlen, [&] {
+        const auto source = ddm::open_frame_source(
+            path, format == 1 ? ddm::StackFormat::PgmDir : ddm::StackFormat::RawStack);
+        ddm::RunConfig config;
+        config.algorithm = algorithm == 0   ? ddm::Algorithm::WithFt
+                           : algorithm == 1 ? ddm::Algorithm::WithoutFt
+                                            : ddm::Algorithm::Direct;
+        config.precision = precision == 0 ? ddm::Precision::F32 : ddm::Precision::F64;
+        config.lags.assign(lags, lags + n_lags);
+        if (has_q_max)
+            config.q_max = q_max;
+        config.memory_bytes = memory_bytes;
+        config.workers = workers;
+        config.out_dir = out_dir;
+        const ddm::ResultArchive archive = ddm::run(*source, config);
+        ddm::write_results(archive, out_dir);
+        const auto wv = ddm::cutoff_set(static_cast<int>(archive.map.width),
+                                        static_cast<int>(archive.map.height), archive.q_max);
+        const ddm::RadialProfile profile = ddm::azimuthal_average(archive.map, wv);
+        ddm::write_radial_csv(profile, std::filesystem::path(out_dir) / "radial.csv");
+        const auto fits = ddm::fit_all_bins(profile);
+        if (!fits.empty())
+            ddm::write_fits_csv(fits, std::filesystem::path(out_dir) / "fits.csv");
     });
 }
 

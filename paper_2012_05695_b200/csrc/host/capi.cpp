@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <filesystem>
 #include <new>
 #include <optional>
 #include <string>
@@ -215,6 +216,21 @@ int ddm_b200_run_pgm_dir(const char* dir, const ddm_b200_run_config* config, dou
         ddm::PgmDirSource src(dir);
         const auto a = ddm::run_into(src, to_config(config), out_values, out_capacity);
         emit(a, out_lags, out_n_lags, counters, timing);
+    });
+}
+
+int ddm_b200_analyze(const char* path, int format, const ddm_b200_run_config* config,
+                     const char* out_dir, int64_t* out_n_lags, int64_t* fits_written,
+                     ddm_b200_counters* counters, ddm_b200_timing* timing) {
+    return guarded([&] {
+        if (!path || !out_dir || !*out_dir) throw ddm::InputError("null path");
+        // `ddm_cli.cpp:103-109`: auto = a directory is a PGM stack, anything else a raw stack
+        const bool pgm = format == 1 || (format < 0 && std::filesystem::is_directory(path));
+        const auto src = ddm::open_frame_source(path, pgm ? ddm::StackFormat::PgmDir
+                                                          : ddm::StackFormat::RawStack);
+        const auto a = ddm::analyze(*src, to_config(config), out_dir);
+        if (fits_written) *fits_written = std::filesystem::exists(std::filesystem::path(out_dir) / "fits.csv");
+        emit(a, nullptr, out_n_lags, counters, timing);
     });
 }
 

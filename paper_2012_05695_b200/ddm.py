@@ -9,6 +9,8 @@ library is missing this module raises on first use.
 from __future__ import annotations
 
 import ctypes as C
+import json
+import os
 from dataclasses import dataclass, field
 from pathlib import Path
 from typing import Callable, Optional, Sequence
@@ -301,6 +303,39 @@ def run_pgm_dir(path: str, config: RunConfig) -> ResultArchive:
                          config.workers,
                          {f: int(getattr(counters, f)) for f, _ in Counters._fields_},
                          {f: float(getattr(timing, f)) for f, _ in Timing._fields_})
+
+
+def analyze(path: str, out: str, config: RunConfig, fmt: str = "auto", lag_spec: str = "all",
+            memory_limit: Optional[str] = None) -> dict:
+    """`ddm analyze` (`tools/ddm_cli.cpp:206-240`): run, write_results, radial.csv, fits.csv
+    (one C-ABI call, ddm_b200_analyze) and the CLI's run.json option echo (`:189-203`).
+
+    `config.lags` is the resolved lag list; `lag_spec` / `memory_limit` are only echoed."""
+    f = {"raw_stack": 0, "pgm_dir": 1, "auto": -1}.get(fmt)
+    if f is None:
+        raise InputError(f"unknown stack format '{fmt}'")
+    os.makedirs(out, exist_ok=True)
+    keep: list = []
+    c = _config(config, keep)
+    n_lags, fits = C.c_int64(0), C.c_int64(0)
+    counters, timing = Counters(), Timing()
+    rc = lib().ddm_b200_analyze(str(path).encode(), f, C.byref(c), str(out).encode(), C.byref(n_lags),
+                                C.byref(fits), C.byref(counters), C.byref(timing))
+    for item in keep:
+        if isinstance(item, list) and item and isinstance(item[0], Exception):
+            raise item[0]
+    _check(rc)
+    resolved = fmt if fmt != "auto" else ("pgm_dir" if os.path.isdir(path) else "raw_stack")
+    echo = {"tool_version": "0.1.0-b200", "input": str(path), "format": resolved, "lags": lag_spec,
+            "q_max": config.q_max, "memory_limit_bytes": int(config.memory_bytes),
+            "workers": int(config.workers), "precision": config.precision, "out": str(out),
+            "subcommand": "analyze", "algorithm": config.algorithm}
+    with open(os.path.join(out, "run.json"), "w") as fh:
+        json.dump(echo, fh, indent=2, sort_keys=True)
+        fh.write("\n")
+    return {"n_lags": n_lags.value, "fits_written": bool(fits.value),
+            "counters": {k: int(getattr(counters, k)) for k, _ in Counters._fields_},
+            "timing": {k: float(getattr(timing, k)) for k, _ in Timing._fields_}}
 
 
 @dataclass

@@ -10,6 +10,7 @@ Inputs are portable: the reference synth generator (mt19937_64 + Box-Muller,
 from __future__ import annotations
 
 import hashlib
+import json
 import sys
 from pathlib import Path
 
@@ -133,8 +134,54 @@ def pairwise() -> None:
     np.savez_compressed(OUT / "pairwise.npz", **out)
 
 
+# `ddm analyze` cases: (name, format, W, H, N, seed, algorithm, precision, lags, q_max)
+ANALYZE_CASES = [
+    ("raw_f64_all", "raw_stack", 32, 24, 48, 31, "with_ft", "f64", (), None),
+    ("pgm_f32_log_qmax", "pgm_dir", 24, 20, 40, 32, "with_ft", "f32", "log", 7.5),
+    ("raw_f64_without", "raw_stack", 20, 16, 30, 33, "without_ft", "f64", (0, 1, 2, 3, 5, 8, 13), None),
+    ("raw_f32_nofits", "raw_stack", 16, 16, 3, 34, "with_ft", "f32", (), None),
+]
+
+
+def write_stack(path: Path, fmt: str, st: np.ndarray, frame_interval: float = 0.25) -> None:
+    """The inputs of ANALYZE_CASES: a raw stack (JSON header line + u16le) or a PGM directory
+    (P5, maxval 65535, big-endian), the formats of `image_stack.cpp`."""
+    n, h, w = st.shape
+    if fmt == "raw_stack":
+        with open(path, "wb") as f:
+            f.write(json.dumps({"width": w, "height": h, "frames": n, "dtype": "u16le",
+                                "frame_interval": frame_interval}).encode() + b"\n")
+            f.write(st.astype("<u2").tobytes())
+    else:
+        path.mkdir(parents=True, exist_ok=True)
+        for i, fr in enumerate(st):
+            (path / f"f{i:05d}.pgm").write_bytes(f"P5\n{w} {h}\n65535\n".encode() + fr.astype(">u2").tobytes())
+
+
+def analyze_case_stack(w, h, n, seed):
+    return ref.generate(w, h, n, particles=30, diffusion=0.4, seed=seed)
+
+
+def analyze() -> None:
+    """Reference `ddm analyze` artefacts for ANALYZE_CASES -> tests/golden/analyze/<case>/."""
+    import shutil
+    import tempfile
+    root = OUT / "analyze"
+    shutil.rmtree(root, ignore_errors=True)
+    for name, fmt, w, h, n, seed, alg, prec, lags, qm in ANALYZE_CASES:
+        st = analyze_case_stack(w, h, n, seed)
+        lag_list = O.log_lags(n) if lags == "log" else list(lags)
+        with tempfile.TemporaryDirectory() as tmp:
+            src = Path(tmp) / ("in" if fmt == "pgm_dir" else "in.raw")
+            write_stack(src, fmt, st)
+            ref.analyze(str(src), str(root / name), fmt, alg, prec, lag_list, qm, workers=2)
+        print(name, sorted(p.name for p in (root / name).iterdir())[:4], "...")
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["pairwise"]:
         pairwise()
+    elif sys.argv[1:] == ["analyze"]:
+        analyze()
     else:
         main()

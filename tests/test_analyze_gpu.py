@@ -1,0 +1,98 @@
+"""`ddm analyze` as a library call (§8f rank 1): ddm_b200_analyze writes the reference CLI's
+artefact set (`proj/tools/ddm_cli.cpp:206-240`) — d_m<lag>.bin + index.json (write_results,
+`archive.cpp:60-110`), radial.csv and fits.csv (`analysis.cpp:273-304`) — and the files are
+compared with the reference library's own output for the same input (tests/golden/analyze,
+written by `make_golden.py analyze` through oracle/ref_capi.cpp:ref_analyze).
+
+Tolerances: maps and ring means 1e-10 relative for f64, relative L2 1e-4 for f32 (north
+star); integer fields (lags, bins, counts, counters, manifest) exact; fits: same rings and
+flags, ok-fit parameters within 1e-6 (f64 maps) / 1e-3 (f32 maps) relative — the device
+LM sums in warp-tree order, the reference sequentially.
+"""
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from golden.artifacts import read_artifacts, stable_index
+from golden.make_golden import ANALYZE_CASES, write_stack
+from oracle import ddm_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+GOLD = Path(__file__).resolve().parent / "golden" / "analyze"
+
+
+@pytest.fixture(scope="module")
+def ddm():
+    from paper_2012_05695_b200 import ddm as D
+    if D.device_count() < 1:
+        pytest.skip("no CUDA device")
+    return D
+
+
+def _analyze(ddm, tmp_path, case):
+    name, fmt, w, h, n, seed, alg, prec, lags, qm = case
+    st = ddm.generate(w, h, n, particles=30, diffusion=0.4, seed=seed)
+    src = tmp_path / ("in" if fmt == "pgm_dir" else "in.raw")
+    write_stack(src, fmt, st)
+    lag_list = O.log_lags(n) if lags == "log" else list(lags)
+    cfg = ddm.RunConfig(algorithm=alg, precision=prec, lags=lag_list, q_max=qm,
+                        memory_bytes=1 << 40, workers=2)
+    out = tmp_path / "out"
+    info = ddm.analyze(str(src), str(out), cfg, fmt="auto")
+    return info, read_artifacts(out), read_artifacts(GOLD / name)
+
+
+@pytest.mark.parametrize("case", ANALYZE_CASES, ids=[c[0] for c in ANALYZE_CASES])
+def test_analyze_artifacts_match_reference(ddm, tmp_path, case):
+    prec_f64 = case[7] == "f64"
+    info, got, ref = _analyze(ddm, tmp_path, case)
+    assert got["files"] == sorted(ref["files"] + ["run.json"])
+    # the workspace is out_dir, so the group partials stay beside the maps (scheduler.cpp:447)
+    ls = lambda d: sorted(p.name for p in (d / "partials").iterdir())  # noqa: E731
+    assert ls(tmp_path / "out") == ls(GOLD / case[0])
+    assert stable_index(got["index"]) == stable_index(ref["index"])
+    assert info["n_lags"] == len(ref["index"]["lags"])
+    assert info["fits_written"] == (ref["fits"] is not None)
+    for m, r in ref["maps"].items():
+        g = got["maps"][m]
+        if prec_f64:
+            assert O.relative_deviation(g, r) <= 1e-10, m
+        else:
+            assert O.relative_l2(g, r) <= 1e-4, m
+    assert [x[:2] + x[3:] for x in got["radial"]] == [x[:2] + x[3:] for x in ref["radial"]]
+    g = np.asarray([x[2] for x in got["radial"]])
+    r = np.asarray([x[2] for x in ref["radial"]])
+    if prec_f64:
+        assert O.relative_deviation(g, r) <= 1e-10
+    else:
+        assert O.relative_l2(g, r) <= 1e-4
+    if ref["fits"] is None:
+        assert got["fits"] is None
+        return
+    assert [(x[0], x[5]) for x in got["fits"]] == [(x[0], x[5]) for x in ref["fits"]]
+    tol = 1e-6 if prec_f64 else 1e-3
+    for gf, rf in zip(got["fits"], ref["fits"]):
+        if rf[5] != "ok":
+            continue
+        scale = max(abs(rf[1]), abs(rf[2]))
+        assert abs(gf[1] - rf[1]) <= tol * scale and abs(gf[2] - rf[2]) <= tol * scale, gf
+        assert abs(gf[3] - rf[3]) <= tol * rf[3], (gf, rf)
+
+
+def test_analyze_run_json_echo(ddm, tmp_path):
+    """The CLI's option echo (`ddm_cli.cpp:189-203`, `:226-229`) beside the artefacts."""
+    case = ANALYZE_CASES[0]
+    _analyze(ddm, tmp_path, case)
+    echo = json.loads((tmp_path / "out" / "run.json").read_text())
+    assert echo["subcommand"] == "analyze" and echo["algorithm"] == "with_ft"
+    assert echo["format"] == "raw_stack" and echo["precision"] == "f64"
+    assert set(echo) == {"tool_version", "input", "format", "lags", "q_max", "memory_limit_bytes",
+                         "workers", "precision", "out", "subcommand", "algorithm"}
+
+
+def test_analyze_rejects_missing_input(ddm, tmp_path):
+    with pytest.raises(ddm.IoError):
+        ddm.analyze(str(tmp_path / "nope.raw"), str(tmp_path / "o"), ddm.RunConfig(), fmt="raw_stack")

@@ -182,3 +182,39 @@ def test_estimate_diffusion_through_the_abi():
     flags = np.array([-1, 0, 0, 2, 0], dtype=np.int32)
     d, used = ddm.estimate_diffusion(taus, flags, 64, 2, 10)
     assert used == 2 and abs(d - 0.3) < 1e-12
+
+
+# ------------------------------------------------------- `ddm analyze` artefacts (goldens)
+
+ANALYZE_GOLD = Path(__file__).resolve().parent / "golden" / "analyze"
+
+
+@pytest.mark.parametrize("case", sorted(p.name for p in ANALYZE_GOLD.iterdir()))
+def test_analyze_golden_restated(case):
+    """The reference's radial.csv / fits.csv (tests/golden/analyze, written by the reference
+    library via oracle/ref_capi.cpp:ref_analyze) follow from its own d_m*.bin maps under the
+    oracle's azimuthal_average and fit_exponential restatements."""
+    from golden.artifacts import read_artifacts
+    a = read_artifacts(ANALYZE_GOLD / case)
+    idx = a["index"]
+    lags = sorted(a["maps"])
+    assert lags == idx["lags"]
+    vals = np.stack([a["maps"][m] for m in lags])
+    means, counts = O.azimuthal_average(vals, idx["width"], idx["height"], idx["q_max"])
+    expect = [(m, b) for m in lags for b in range(len(counts)) if counts[b] > 0]
+    assert [(r[0], r[1]) for r in a["radial"]] == expect
+    for (m, b, mean, cnt) in a["radial"]:
+        assert cnt == counts[b]
+        assert abs(mean - means[lags.index(m), b]) <= 1e-12 * max(abs(mean), 1e-300)
+    usable = [i for i, m in enumerate(lags) if m >= 1]
+    if len(usable) < 4:
+        assert a["fits"] is None
+        return
+    t = np.asarray([lags[i] for i in usable], float) * idx["frame_interval"]
+    fitted = [b for b in range(len(counts)) if counts[b] > 0]
+    assert [r[0] for r in a["fits"]] == fitted
+    for (b, A, B, tau, res, flag) in a["fits"]:
+        oA, oB, otau, ores, oflag = O.fit_exponential(t, means[usable, b], idx["frame_interval"])
+        assert oflag == flag, (b, flag, oflag)
+        if flag == "ok":
+            assert abs(otau - tau) <= 1e-6 * tau and abs(ores - res) <= 1e-6 * max(res, 1e-300)
