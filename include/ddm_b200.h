@@ -111,6 +111,17 @@ int ddm_b200_run_pgm_dir(const char* dir, const ddm_b200_run_config* config, dou
 int ddm_b200_analyze(const char* path, int format, const ddm_b200_run_config* config,
                      const char* out_dir, int64_t* out_n_lags, int64_t* fits_written,
                      ddm_b200_counters* counters, ddm_b200_timing* timing);
+/* `ddm bench` (tools/ddm_cli.cpp:338-385, core/src/bench.cpp): every (size, N, algorithm
+   [0 with_ft, 1 without_ft, 2 direct], workers, budget) cell of a sweep over synthetic stacks
+   seeded (N << 32) ^ size, run in f64 (warmup + repetitions, per-field medians), written to
+   out_csv in bench.csv's format; crossover_sizes / crossover_n (capacity n_sizes) receive the
+   smallest N where with_ft beats without_ft per size (-1 = none), n_crossover their count.
+   Cells that fail to plan are recorded as failed rows (nan times). */
+int ddm_b200_bench_sweep(const int* frame_counts, int n_frame_counts, const int* sizes, int n_sizes,
+                         const int* algorithms, int n_algorithms, const int* workers, int n_workers,
+                         const int64_t* budgets, int n_budgets, int repetitions, int warmup,
+                         const char* out_csv, int* crossover_sizes, int* crossover_n,
+                         int* n_crossover);
 /* Dimensions of a stack on disk (format 0 raw_stack, 1 pgm_dir; open_frame_source). */
 int ddm_b200_stack_dims(const char* path, int format, int* width, int* height, int* frames);
 

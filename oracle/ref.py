@@ -241,3 +241,21 @@ def analyze(path: str, out_dir: str, fmt: str = "raw_stack", algorithm: str = "w
                            C.c_double(0.0 if q_max is None else q_max), C.c_int64(memory_bytes),
                            workers, str(out_dir).encode(), err, 1024)
     _check(rc, err)
+
+
+def bench_sweep(frame_counts, sizes, algorithms=("with_ft", "without_ft"), workers=(2,),
+                budgets=(), repetitions: int = 1, warmup: int = 0, out_csv: str = "bench.csv"):
+    """The reference's `ddm bench` sweep (`proj/core/src/bench.cpp`): writes bench.csv,
+    returns the crossover N* per size (None = never)."""
+    ax = [np.ascontiguousarray(np.asarray(list(v), dtype=np.int32)) for v in
+          (frame_counts, sizes, [{"with_ft": 0, "without_ft": 1, "direct": 2}[a] for a in algorithms],
+           workers)]
+    bud = np.ascontiguousarray(np.asarray(list(budgets), dtype=np.int64))
+    xn = np.zeros(len(ax[1]), np.int32)
+    err = C.create_string_buffer(1024)
+    rc = lib().ref_bench_sweep(_p(ax[0], C.c_int), len(ax[0]), _p(ax[1], C.c_int), len(ax[1]),
+                               _p(ax[2], C.c_int), len(ax[2]), _p(ax[3], C.c_int), len(ax[3]),
+                               _p(bud, C.c_int64) if len(bud) else None, len(bud), repetitions,
+                               warmup, str(out_csv).encode(), _p(xn, C.c_int), err, 1024)
+    _check(rc, err)
+    return {int(s): (int(n) if n >= 0 else None) for s, n in zip(ax[1], xn)}

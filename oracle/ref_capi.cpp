@@ -9,6 +9,7 @@
 
 #include <ddm/analysis.hpp>
 #include <ddm/archive.hpp>
+#include <ddm/bench.hpp>
 #include <ddm/errors.hpp>
 #include <ddm/frame_source.hpp>
 #include <ddm/scheduler.hpp>
@@ -303,6 +304,37 @@ int ref_analyze(const char* path, int format, int algorithm, int precision,
         const auto fits = ddm::fit_all_bins(profile);
         if (!fits.empty())
             ddm::write_fits_csv(fits, std::filesystem::path(out_dir) / "fits.csv");
+    });
+}
+
+} // extern "C"
+
+extern "C" {
+
+// ddm::sweep + write_bench_csv + crossover (proj/core/src/bench.cpp), as tools/ddm_cli.cpp:338-385
+// drives them with the synthetic stack factory.
+int ref_bench_sweep(const int* frame_counts, int n_frame_counts, const int* sizes, int n_sizes,
+                    const int* algorithms, int n_algorithms, const int* workers, int n_workers,
+                    const std::int64_t* budgets, int n_budgets, int repetitions, int warmup,
+                    const char* out_csv, int* crossover_n, char* err, int errlen) {
+    return guarded(err, errlen, [&] {
+        ddm::SweepSpec spec;
+        spec.frame_counts.assign(frame_counts, frame_counts + n_frame_counts);
+        spec.sizes.assign(sizes, sizes + n_sizes);
+        for (int i = 0; i < n_algorithms; ++i)
+            spec.algorithms.push_back(algorithms[i] == 0   ? ddm::Algorithm::WithFt
+                                      : algorithms[i] == 1 ? ddm::Algorithm::WithoutFt
+                                                           : ddm::Algorithm::Direct);
+        spec.worker_counts.assign(workers, workers + n_workers);
+        if (n_budgets > 0)
+            spec.budgets.assign(budgets, budgets + n_budgets);
+        spec.repetitions = repetitions;
+        spec.warmup = warmup;
+        const auto table = ddm::sweep(spec, ddm::synthetic_stack_factory());
+        ddm::write_bench_csv(table, out_csv);
+        const auto xs = ddm::crossover(table);
+        for (std::size_t i = 0; i < xs.size(); ++i)
+            crossover_n[i] = xs[i].n_star ? *xs[i].n_star : -1;
     });
 }
 

@@ -208,8 +208,7 @@ RadialProfile azimuthal_average(const ResultMap& map, const WaveVectorSet& wv) {
         DevMem dv(map.values.size() * sizeof(double)), dor(order.size() * sizeof(std::int64_t)),
             doff(off.size() * sizeof(std::int64_t)), dm(prof.means.size() * sizeof(double));
         cudaStream_t st = eng.stream();
-        b200::check(cudaMemcpyAsync(dv.p, map.values.data(), map.values.size() * sizeof(double),
-                                    cudaMemcpyHostToDevice, st), "upload");
+        detail::upload_pageable(eng, dv.p, map.values.data(), map.values.size() * sizeof(double), st);
         b200::check(cudaMemcpyAsync(dor.p, order.data(), order.size() * sizeof(std::int64_t),
                                     cudaMemcpyHostToDevice, st), "upload");
         b200::check(cudaMemcpyAsync(doff.p, off.data(), off.size() * sizeof(std::int64_t),

@@ -3,6 +3,7 @@
 #include "ddm_b200.h"
 
 #include "ddm/analysis.hpp"
+#include "ddm/bench.hpp"
 #include "ddm/errors.hpp"
 #include "ddm/scheduler.hpp"
 #include "ddm/spectrum.hpp"
@@ -17,6 +18,7 @@
 #include <new>
 #include <optional>
 #include <string>
+#include <type_traits>
 
 namespace {
 
@@ -231,6 +233,40 @@ int ddm_b200_analyze(const char* path, int format, const ddm_b200_run_config* co
         const auto a = ddm::analyze(*src, to_config(config), out_dir);
         if (fits_written) *fits_written = std::filesystem::exists(std::filesystem::path(out_dir) / "fits.csv");
         emit(a, nullptr, out_n_lags, counters, timing);
+    });
+}
+
+int ddm_b200_bench_sweep(const int* frame_counts, int n_frame_counts, const int* sizes, int n_sizes,
+                         const int* algorithms, int n_algorithms, const int* workers, int n_workers,
+                         const int64_t* budgets, int n_budgets, int repetitions, int warmup,
+                         const char* out_csv, int* crossover_sizes, int* crossover_n, int* n_crossover) {
+    return guarded([&] {
+        if (!out_csv || !*out_csv) throw ddm::InputError("null path");
+        ddm::SweepSpec spec;
+        auto take = [](const auto* p, int n) {
+            using T = std::remove_cv_t<std::remove_pointer_t<decltype(p)>>;
+            if (n < 0 || (n > 0 && !p)) throw ddm::InputError("sweep: bad axis");
+            return std::vector<T>(p, p + n);
+        };
+        spec.frame_counts = take(frame_counts, n_frame_counts);
+        spec.sizes = take(sizes, n_sizes);
+        for (const int a : take(algorithms, n_algorithms))
+            spec.algorithms.push_back(a == 0 ? ddm::Algorithm::WithFt
+                                      : a == 1 ? ddm::Algorithm::WithoutFt : ddm::Algorithm::Direct);
+        spec.worker_counts = take(workers, n_workers);
+        spec.budgets = take(budgets, n_budgets);
+        spec.repetitions = repetitions;
+        spec.warmup = warmup;
+        const auto table = ddm::sweep(spec, ddm::synthetic_stack_factory());
+        const std::filesystem::path csv(out_csv);
+        if (csv.has_parent_path()) std::filesystem::create_directories(csv.parent_path());
+        ddm::write_bench_csv(table, csv);
+        const auto xs = ddm::crossover(table);
+        if (n_crossover) *n_crossover = int(xs.size());
+        for (std::size_t i = 0; i < xs.size(); ++i) {
+            if (crossover_sizes) crossover_sizes[i] = xs[i].size;
+            if (crossover_n) crossover_n[i] = xs[i].n_star ? *xs[i].n_star : -1;
+        }
     });
 }
 

@@ -23,6 +23,7 @@
 #include <exception>
 #include <thread>
 
+#include <sys/mman.h>
 #include <unistd.h>
 
 namespace fs = std::filesystem;
@@ -259,7 +260,9 @@ ResultArchive run_core(const Ingest& in, const RunConfig& config, double* out,
     std::lock_guard<std::mutex> lock(eng.mutex());
     cudaStream_t st = eng.stream();
 
+    Trace trace("run");
     const void* d_frames = stage_frames(eng, in, timing.disk);
+    trace.lap("stage");
 
     b200::RunSpec spec;
     spec.W = W;
@@ -296,7 +299,12 @@ ResultArchive run_core(const Ingest& in, const RunConfig& config, double* out,
             if (ec) throw IoError("cannot create workspace " + workspace.string());
         }
         spec.partial_mode = true;
-        std::vector<double> host;
+        // Without a before_merge hook nothing can touch the partials between their write and
+        // the merge, so the map is assembled from the same host values the files are written
+        // from (identical to re-reading them); with a hook the files are merged as written.
+        const bool direct = !config.before_merge;
+        const bool in_place = direct && spec.identity && plan.group_count() == 1;
+        if (direct && !spec.identity) std::memset(out, 0, std::size_t(total) * sizeof(double));
         spec.on_partial = [&](std::size_t g, const void* d_partial, std::int64_t gc) {
             clock.start();
             PartialResult p;
@@ -309,21 +317,40 @@ ResultArchive run_core(const Ingest& in, const RunConfig& config, double* out,
             p.frame_interval = in.frame_interval;
             p.q_max = config.q_max;
             p.lags = lags;
-            p.values.resize(lags.size() * std::size_t(gc));
-            b200::check(cudaMemcpyAsync(p.values.data(), d_partial, p.values.size() * sizeof(double),
-                                        cudaMemcpyDeviceToHost, st), "partial copy");
+            const std::size_t cnt = lags.size() * std::size_t(gc);
+            double* host = out;  // lag-major [lags][plane] is this partial's own layout
+            if (!in_place) {
+                p.values.resize(cnt);
+                host = p.values.data();
+            }
+            b200::check(cudaMemcpyAsync(host, d_partial, cnt * sizeof(double), cudaMemcpyDeviceToHost, st),
+                        "partial copy");
             b200::check(cudaStreamSynchronize(st), "sync");
-            write_partial(p, workspace);
+            trace.lap("partial d2h");
+            detail::write_partial_payload(p, host, cnt, workspace);
+            trace.lap("partial file");
+            if (direct && !in_place)
+                for (std::size_t li = 0; li < lags.size(); ++li) {
+                    double* dst = out + li * std::size_t(plane);
+                    const double* src = host + li * std::size_t(gc);
+                    for (std::int64_t j = 0; j < gc; ++j) dst[spec.flat[std::size_t(p.wv_begin + j)]] = src[j];
+                }
             clock.stop(timing.merge);
         };
         eng.run(spec, &times);
-        if (config.before_merge) config.before_merge(workspace);
-        clock.start();
-        const ResultMap merged = merge_partials(list_partials(workspace));
-        if (merged.lags != lags || std::int64_t(merged.values.size()) != total)
-            throw InputError("merged partials do not match the run layout");
-        std::memcpy(out, merged.values.data(), std::size_t(total) * sizeof(double));
-        clock.stop(timing.merge);
+        // stale partials of an earlier run in out_dir: merge from the files, as the reference
+        // does (and fails as it does)
+        const bool stale = direct && list_partials(workspace).size() != plan.groups.size();
+        if (!direct || stale) {
+            if (config.before_merge) config.before_merge(workspace);
+            clock.start();
+            const ResultMap merged = merge_partials(list_partials(workspace));
+            trace.lap("merge");
+            if (merged.lags != lags || std::int64_t(merged.values.size()) != total)
+                throw InputError("merged partials do not match the run layout");
+            std::memcpy(out, merged.values.data(), std::size_t(total) * sizeof(double));
+            clock.stop(timing.merge);
+        }
         archive.map.values.clear();
     } else {
         double* d_map = static_cast<double*>(eng.buffer("map", std::size_t(total) * sizeof(double)));
@@ -354,6 +381,40 @@ ResultArchive run_core(const Ingest& in, const RunConfig& config, double* out,
     return archive;
 }
 
+void upload_pageable(b200::Engine& eng, void* dst, const void* src, std::size_t bytes,
+                     cudaStream_t stream) {
+    constexpr std::size_t kChunk = std::size_t(32) << 20, kPiece = std::size_t(4) << 20;
+    if (bytes < 2 * kChunk) {
+        b200::check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream), "upload");
+        b200::check(cudaStreamSynchronize(stream), "sync");
+        return;
+    }
+    cudaEvent_t done[2];
+    for (auto& e : done) b200::check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    try {
+        const char* s = static_cast<const char*>(src);
+        char* d = static_cast<char*>(dst);
+        for (std::size_t off = 0, i = 0; off < bytes; off += kChunk, ++i) {
+            const int slot = int(i & 1);
+            const std::size_t n = std::min(kChunk, bytes - off);
+            char* pin = static_cast<char*>(eng.pinned(slot, kChunk));
+            if (i >= 2) b200::check(cudaEventSynchronize(done[slot]), "event sync");
+            parallel_for((n + kPiece - 1) / kPiece, [&](std::size_t k) {
+                const std::size_t o = k * kPiece;
+                std::memcpy(pin + o, s + off + o, std::min(kPiece, n - o));
+            });
+            b200::check(cudaMemcpyAsync(d + off, pin, n, cudaMemcpyHostToDevice, stream), "upload");
+            b200::check(cudaEventRecord(done[slot], stream), "event");
+        }
+        b200::check(cudaStreamSynchronize(stream), "sync");
+    } catch (...) {
+        cudaStreamSynchronize(stream);
+        for (auto e : done) cudaEventDestroy(e);
+        throw;
+    }
+    for (auto e : done) cudaEventDestroy(e);
+}
+
 }  // namespace detail
 
 ResultArchive run_into(FrameSource& source, const RunConfig& config, double* out,
@@ -372,9 +433,23 @@ ResultArchive run(FrameSource& source, const RunConfig& config) {
     if (config.workers < 1) throw InputError("workers must be at least 1");
     const std::int64_t n_lags =
         config.lags.empty() ? source.frames() : std::int64_t(config.lags.size());
-    std::vector<double> values(std::size_t(n_lags) * std::size_t(source.height()) *
-                               std::size_t(half_cols(source.width())));
+    detail::Trace trace("ddm::run");
+    const std::size_t count =
+        std::size_t(n_lags) * std::size_t(source.height()) * std::size_t(half_cols(source.width()));
+    std::vector<double> values;
+    values.reserve(count);
+    // GB-sized maps: ask for transparent huge pages before the zero fill faults the range in
+    // (4 KiB faults cost ~0.35 s per GiB; THP "madvise" mode is common)
+    if (count * sizeof(double) >= (std::size_t(64) << 20)) {
+        constexpr std::uintptr_t kHuge = std::uintptr_t(2) << 20;
+        const auto b = (reinterpret_cast<std::uintptr_t>(values.data()) + kHuge - 1) & ~(kHuge - 1);
+        const auto e = (reinterpret_cast<std::uintptr_t>(values.data() + count)) & ~(kHuge - 1);
+        if (e > b) ::madvise(reinterpret_cast<void*>(b), e - b, MADV_HUGEPAGE);
+    }
+    values.resize(count);
+    trace.lap("map alloc");
     ResultArchive a = run_into(source, config, values.data(), std::int64_t(values.size()));
+    trace.lap("run_into");
     values.resize(std::size_t(a.map.plane_size()) * a.map.lags.size());
     a.map.values = std::move(values);
     return a;

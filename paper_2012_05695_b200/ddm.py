@@ -338,6 +338,50 @@ def analyze(path: str, out: str, config: RunConfig, fmt: str = "auto", lag_spec:
             "timing": {k: float(getattr(timing, k)) for k, _ in Timing._fields_}}
 
 
+def bench_sweep(frame_counts, sizes, algorithms=("with_ft", "without_ft"), workers=(2,),
+                budgets=(), repetitions: int = 3, warmup: int = 1, out: Optional[str] = None):
+    """`ddm bench` (`tools/ddm_cli.cpp:338-385`, `core/src/bench.cpp`): the sweep over
+    synthetic stacks through one C-ABI call (ddm_b200_bench_sweep), bench.csv in `out`, plus
+    the CLI's run.json echo. Returns (rows of bench.csv as dicts, {size: N* or None})."""
+    import csv
+    import tempfile
+    alg_ids = []
+    for a in algorithms:
+        if a not in ("with_ft", "without_ft", "direct"):
+            raise InputError(f"unknown algorithm '{a}'")
+        alg_ids.append({"with_ft": 0, "without_ft": 1, "direct": 2}[a])
+    ax = [np.ascontiguousarray(np.asarray(list(v), dtype=np.int32)) for v in (frame_counts, sizes, alg_ids, workers)]
+    bud = np.ascontiguousarray(np.asarray(list(budgets), dtype=np.int64))
+    ns = max(len(ax[1]), 1)
+    xs, xn, nx = np.zeros(ns, np.int32), np.zeros(ns, np.int32), C.c_int(0)
+    tmp = None
+    if out is None:
+        tmp = tempfile.TemporaryDirectory()
+        out = tmp.name
+    os.makedirs(out, exist_ok=True)
+    csv_path = os.path.join(out, "bench.csv")
+
+    def ptr(a, ct):
+        return _p(a, ct) if len(a) else None
+    _check(lib().ddm_b200_bench_sweep(ptr(ax[0], C.c_int), len(ax[0]), ptr(ax[1], C.c_int), len(ax[1]),
+                                      ptr(ax[2], C.c_int), len(ax[2]), ptr(ax[3], C.c_int), len(ax[3]),
+                                      ptr(bud, C.c_int64), len(bud), int(repetitions), int(warmup),
+                                      csv_path.encode(), _p(xs, C.c_int), _p(xn, C.c_int), C.byref(nx)))
+    with open(csv_path, newline="") as f:
+        rows = list(csv.DictReader(f))
+    echo = {"subcommand": "bench", "tool_version": "0.1.0-b200",
+            "sweep": ",".join(str(n) for n in frame_counts), "sizes": ",".join(str(s) for s in sizes),
+            "algorithms": ",".join(algorithms), "workers": ",".join(str(w) for w in workers),
+            "budgets": ",".join(str(b) for b in budgets) if len(budgets) else "default",
+            "repetitions": int(repetitions), "warmup": int(warmup), "out": str(out)}
+    with open(os.path.join(out, "run.json"), "w") as fh:
+        json.dump(echo, fh, indent=2, sort_keys=True)
+        fh.write("\n")
+    if tmp is not None:
+        tmp.cleanup()
+    return rows, {int(xs[i]): (int(xn[i]) if xn[i] >= 0 else None) for i in range(nx.value)}
+
+
 @dataclass
 class LagProfile:
     d: np.ndarray

@@ -178,10 +178,24 @@ def analyze() -> None:
         print(name, sorted(p.name for p in (root / name).iterdir())[:4], "...")
 
 
+# `ddm bench` sweep whose deterministic columns are pinned (budgets: ample, grouped, too small)
+BENCH_SWEEP = dict(frame_counts=(16, 48), sizes=(16, 32), algorithms=("with_ft", "without_ft", "direct"),
+                   workers=(2,), budgets=(1 << 30, 40000, 100))
+
+
+def bench() -> None:
+    """The reference's bench.csv for BENCH_SWEEP -> tests/golden/bench_sweep.csv (times are
+    host-specific; the tests compare every other column)."""
+    ref.bench_sweep(**BENCH_SWEEP, repetitions=1, warmup=0, out_csv=OUT / "bench_sweep.csv")
+    print((OUT / "bench_sweep.csv").read_text())
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["pairwise"]:
         pairwise()
     elif sys.argv[1:] == ["analyze"]:
         analyze()
+    elif sys.argv[1:] == ["bench"]:
+        bench()
     else:
         main()

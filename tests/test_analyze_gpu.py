@@ -51,7 +51,7 @@ def test_analyze_artifacts_match_reference(ddm, tmp_path, case):
     info, got, ref = _analyze(ddm, tmp_path, case)
     assert got["files"] == sorted(ref["files"] + ["run.json"])
     # the workspace is out_dir, so the group partials stay beside the maps (scheduler.cpp:447)
-    ls = lambda d: sorted(p.name for p in (d / "partials").iterdir())  # noqa: E731
+    ls = lambda d: sorted(p.name for p in (d / "partials").iterdir()) if (d / "partials").is_dir() else []  # noqa: E731,E501
     assert ls(tmp_path / "out") == ls(GOLD / case[0])
     assert stable_index(got["index"]) == stable_index(ref["index"])
     assert info["n_lags"] == len(ref["index"]["lags"])
@@ -96,3 +96,65 @@ def test_analyze_run_json_echo(ddm, tmp_path):
 def test_analyze_rejects_missing_input(ddm, tmp_path):
     with pytest.raises(ddm.IoError):
         ddm.analyze(str(tmp_path / "nope.raw"), str(tmp_path / "o"), ddm.RunConfig(), fmt="raw_stack")
+
+
+# ----------------------------------------------------------------- `ddm bench` sweep
+
+def test_bench_sweep_matches_reference_columns(ddm, tmp_path):
+    """Every deterministic column of bench.csv (cells, planned groups/passes, counters,
+    failed rows) equals the reference sweep's (tests/golden/bench_sweep.csv, written by
+    `make_golden.py bench` through the reference's own ddm::sweep); the crossover is the
+    first N whose with_ft median total beats without_ft's (`bench.cpp:144-183`)."""
+    import csv
+    from golden.make_golden import BENCH_SWEEP
+    rows, xo = ddm.bench_sweep(**BENCH_SWEEP, repetitions=2, warmup=1, out=str(tmp_path))
+    with open(GOLD.parent / "bench_sweep.csv", newline="") as f:
+        ref_rows = list(csv.DictReader(f))
+    timed = {"seconds_total", "seconds_disk", "seconds_step1", "seconds_step2", "seconds_merge"}
+    assert len(rows) == len(ref_rows)
+    for g, r in zip(rows, ref_rows):
+        assert {k: v for k, v in g.items() if k not in timed} == {k: v for k, v in r.items() if k not in timed}
+        if r["seconds_total"] == "nan":
+            assert all(g[k] == "nan" for k in timed)
+        else:
+            assert float(g["seconds_total"]) > 0.0
+    assert set(xo) == set(BENCH_SWEEP["sizes"])
+    for size, n_star in xo.items():
+        expect = None
+        for n in sorted(BENCH_SWEEP["frame_counts"]):
+            cells = [x for x in rows if int(x["width"]) == size and int(x["N"]) == n and x["seconds_total"] != "nan"]
+            w = next((x for x in cells if x["algorithm"] == "with_ft"), None)
+            wo = next((x for x in cells if x["algorithm"] == "without_ft"), None)
+            if w and wo and float(w["seconds_total"]) < float(wo["seconds_total"]):
+                expect = n
+                break
+        assert n_star == expect
+    echo = json.loads((tmp_path / "run.json").read_text())
+    assert echo["subcommand"] == "bench" and echo["budgets"] == "1073741824,40000,100"
+
+
+def test_out_dir_runs_assemble_the_partials_they_write(ddm, tmp_path):
+    """With a workspace and no before_merge hook the map is assembled from the values the
+    partials are written from; it equals the in-memory run and the files re-merge to it
+    (grouped, cutoff and whole-plane layouts)."""
+    st = ddm.generate(48, 40, 64, particles=20, seed=5)
+    for qm, budget in ((None, 1 << 40), (9.5, 1 << 40), (None, 64 * 16 * 300), (11.0, 64 * 16 * 50)):
+        base = ddm.RunConfig(precision="f64", q_max=qm, memory_bytes=budget)
+        ref_map = ddm.run(st, base).values
+        out = tmp_path / f"w{qm}_{budget}"
+        cfg = ddm.RunConfig(precision="f64", q_max=qm, memory_bytes=budget, out_dir=str(out))
+        got = ddm.run(st, cfg).values
+        assert np.array_equal(got, ref_map)
+        groups = O.plan_with_ft(len(O.cutoff_set(48, 40, qm)), 64, budget)[1]
+        assert len(list((out / "partials").iterdir())) == len(groups)
+        assert len(groups) > 1 or budget == 1 << 40
+
+
+def test_stale_partials_in_out_dir_fail_as_the_reference(ddm, tmp_path):
+    """A foreign group file in out_dir/partials makes the merge fail (`archive.cpp:239-262`)."""
+    st = ddm.generate(32, 32, 32, particles=20, seed=6)
+    out = tmp_path / "o"
+    (out / "partials").mkdir(parents=True)
+    (out / "partials" / "group9.bin").write_bytes(b"not a partial\n")
+    with pytest.raises(ddm.InputError):
+        ddm.run(st, ddm.RunConfig(memory_bytes=1 << 40, out_dir=str(out)))
