@@ -103,6 +103,10 @@ ResultMap merge_partials(const std::vector<std::filesystem::path>& files);
 /// (radial.csv) and the ring fits (fits.csv). The CLI's own run.json echo is not written.
 ResultArchive analyze(FrameSource& source, RunConfig config, const std::filesystem::path& out_dir);
 
+struct CompareReport;
+/// `ddm compare` as a library call: `config` with each algorithm in turn (analysis.hpp).
+CompareReport compare(FrameSource& source, const RunConfig& config, Algorithm a, Algorithm b);
+
 } // namespace ddm
 
 #endif

@@ -7,6 +7,7 @@
 #include "ddm/image_stack.hpp"
 
 #include <cstdint>
+#include <filesystem>
 
 namespace ddm {
 
@@ -25,6 +26,10 @@ struct SynthConfig {
 };
 
 ImageStack generate(const SynthConfig& config);
+
+/// synth.json beside a generated stack (`synth.cpp:134-155`): tool version, generator name and
+/// every SynthConfig field.
+void write_synth_manifest(const SynthConfig& config, const std::filesystem::path& path);
 
 } // namespace ddm
 

@@ -122,6 +122,19 @@ int ddm_b200_bench_sweep(const int* frame_counts, int n_frame_counts, const int*
                          const int64_t* budgets, int n_budgets, int repetitions, int warmup,
                          const char* out_csv, int* crossover_sizes, int* crossover_n,
                          int* n_crossover);
+/* `ddm compare` (tools/ddm_cli.cpp:247-290): the stack through two algorithms (0 with_ft,
+   1 without_ft, 2 direct) with `config` otherwise; deviation = max|a-b| / max(|a|,|b|),
+   tolerance 1e-4 (f32) / 1e-9 (f64), pass = deviation <= tolerance.  The CLI's compare.json
+   is the caller's (the Python wrapper writes it). */
+int ddm_b200_compare(const char* path, int format, const ddm_b200_run_config* config, int algorithm_a,
+                     int algorithm_b, double* deviation, double* tolerance, int* pass,
+                     ddm_b200_timing* timing_a, ddm_b200_timing* timing_b);
+/* `ddm synth` (tools/ddm_cli.cpp:306-327): generate a size x size stack (synth.cpp:98-132) and
+   write out_dir/stack.raw (write_raw_stack, image_stack.cpp:223-247) and out_dir/synth.json
+   (write_synth_manifest, synth.cpp:134-155). Host only. */
+int ddm_b200_synth(const char* out_dir, int64_t particles, double diffusion, double psf_sigma,
+                   double amplitude, double background, int size, int frames, double frame_interval,
+                   uint64_t seed);
 /* Dimensions of a stack on disk (format 0 raw_stack, 1 pgm_dir; open_frame_source). */
 int ddm_b200_stack_dims(const char* path, int format, int* width, int* height, int* frames);
 

@@ -150,3 +150,31 @@ ResultArchive analyze(FrameSource& source, RunConfig config, const fs::path& out
 }
 
 }  // namespace ddm
+
+namespace ddm {
+
+double relative_deviation(const ResultMap& a, const ResultMap& b) {
+    double peak = 0.0;
+    for (const double v : a.values) peak = std::max(peak, std::abs(v));
+    for (const double v : b.values) peak = std::max(peak, std::abs(v));
+    return peak == 0.0 ? 0.0 : max_abs_difference(a, b) / peak;
+}
+
+CompareReport compare(FrameSource& source, const RunConfig& config, Algorithm a, Algorithm b) {
+    CompareReport r;
+    ResultArchive out[2];
+    const Algorithm algs[2] = {a, b};
+    for (int i = 0; i < 2; ++i) {
+        RunConfig c = config;
+        c.algorithm = algs[i];
+        out[i] = run(source, c);
+        r.algorithms[i] = out[i].algorithm;
+        r.timing[i] = out[i].timing;
+    }
+    r.deviation = relative_deviation(out[0].map, out[1].map);
+    r.tolerance = config.precision == Precision::F32 ? 1e-4 : 1e-9;
+    r.pass = r.deviation <= r.tolerance;
+    return r;
+}
+
+}  // namespace ddm

@@ -13,6 +13,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <random>
 
@@ -306,6 +307,19 @@ ImageStack generate(const SynthConfig& c) {
         splat(xs, ys, c, st.frame(n).data(), canvas);
     }
     return st;
+}
+
+void write_synth_manifest(const SynthConfig& c, const std::filesystem::path& path) {
+    std::FILE* f = std::fopen(path.c_str(), "wb");
+    if (!f) throw IoError("cannot open " + path.string() + " for writing");
+    std::fprintf(f,
+                 "{\n  \"amplitude\": %.17g,\n  \"background\": %.17g,\n  \"diffusion\": %.17g,\n"
+                 "  \"frame_interval\": %.17g,\n  \"frames\": %d,\n  \"generator\": \"mt19937_64/box-muller\",\n"
+                 "  \"height\": %d,\n  \"particles\": %lld,\n  \"psf_sigma\": %.17g,\n  \"seed\": %llu,\n"
+                 "  \"tool_version\": \"0.1.0-b200\",\n  \"width\": %d\n}\n",
+                 c.amplitude, c.background, c.diffusion, c.frame_interval, c.frames, c.height,
+                 (long long)c.particles, c.psf_sigma, (unsigned long long)c.seed, c.width);
+    if (std::fclose(f) != 0) throw IoError("write failed for " + path.string());
 }
 
 }  // namespace ddm

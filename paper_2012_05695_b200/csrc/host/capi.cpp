@@ -5,6 +5,7 @@
 #include "ddm/analysis.hpp"
 #include "ddm/bench.hpp"
 #include "ddm/errors.hpp"
+#include "ddm/image_stack.hpp"
 #include "ddm/scheduler.hpp"
 #include "ddm/spectrum.hpp"
 #include "ddm/synth.hpp"
@@ -267,6 +268,58 @@ int ddm_b200_bench_sweep(const int* frame_counts, int n_frame_counts, const int*
             if (crossover_sizes) crossover_sizes[i] = xs[i].size;
             if (crossover_n) crossover_n[i] = xs[i].n_star ? *xs[i].n_star : -1;
         }
+    });
+}
+
+int ddm_b200_compare(const char* path, int format, const ddm_b200_run_config* config, int algorithm_a,
+                     int algorithm_b, double* deviation, double* tolerance, int* pass,
+                     ddm_b200_timing* timing_a, ddm_b200_timing* timing_b) {
+    return guarded([&] {
+        if (!path) throw ddm::InputError("null path");
+        const bool pgm = format == 1 || (format < 0 && std::filesystem::is_directory(path));
+        const auto src = ddm::open_frame_source(path, pgm ? ddm::StackFormat::PgmDir
+                                                          : ddm::StackFormat::RawStack);
+        auto alg = [](int a) {
+            if (a < 0 || a > 2) throw ddm::InputError("unknown algorithm");
+            return a == 0 ? ddm::Algorithm::WithFt : a == 1 ? ddm::Algorithm::WithoutFt : ddm::Algorithm::Direct;
+        };
+        const auto r = ddm::compare(*src, to_config(config), alg(algorithm_a), alg(algorithm_b));
+        if (deviation) *deviation = r.deviation;
+        if (tolerance) *tolerance = r.tolerance;
+        if (pass) *pass = r.pass ? 1 : 0;
+        ddm_b200_timing* t[2] = {timing_a, timing_b};
+        for (int i = 0; i < 2; ++i)
+            if (t[i]) {
+                t[i]->disk = r.timing[i].disk;
+                t[i]->step1 = r.timing[i].step1;
+                t[i]->step2 = r.timing[i].step2;
+                t[i]->merge = r.timing[i].merge;
+                t[i]->other = r.timing[i].other;
+                t[i]->total = r.timing[i].total;
+            }
+    });
+}
+
+int ddm_b200_synth(const char* out_dir, int64_t particles, double diffusion, double psf_sigma,
+                   double amplitude, double background, int size, int frames, double frame_interval,
+                   uint64_t seed) {
+    return guarded([&] {
+        if (!out_dir || !*out_dir) throw ddm::InputError("null path");
+        ddm::SynthConfig c;
+        c.particles = particles;
+        c.diffusion = diffusion;
+        c.psf_sigma = psf_sigma;
+        c.amplitude = amplitude;
+        c.background = background;
+        c.width = c.height = size;
+        c.frames = frames;
+        c.frame_interval = frame_interval;
+        c.seed = seed;
+        const ddm::ImageStack st = ddm::generate(c);
+        const std::filesystem::path out(out_dir);
+        std::filesystem::create_directories(out);
+        ddm::write_raw_stack(st, out / "stack.raw");
+        ddm::write_synth_manifest(c, out / "synth.json");
     });
 }
 

@@ -382,6 +382,49 @@ def bench_sweep(frame_counts, sizes, algorithms=("with_ft", "without_ft"), worke
     return rows, {int(xs[i]): (int(xn[i]) if xn[i] >= 0 else None) for i in range(nx.value)}
 
 
+def compare(path: str, config: RunConfig, algorithms=("with_ft", "without_ft"), fmt: str = "auto",
+            out: Optional[str] = None) -> dict:
+    """`ddm compare` (`tools/ddm_cli.cpp:247-290`) through ddm_b200_compare; with `out`, the
+    CLI's compare.json report is written there."""
+    ids = {"with_ft": 0, "without_ft": 1, "direct": 2}
+    if len(algorithms) != 2:
+        raise InputError("--algorithms needs exactly two names")
+    for a in algorithms:
+        if a not in ids:
+            raise InputError(f"unknown algorithm '{a}'")
+    f = {"raw_stack": 0, "pgm_dir": 1, "auto": -1}.get(fmt)
+    if f is None:
+        raise InputError(f"unknown stack format '{fmt}'")
+    keep: list = []
+    c = _config(config, keep)
+    dev, tol, ok = C.c_double(0.0), C.c_double(0.0), C.c_int(0)
+    ta, tb = Timing(), Timing()
+    _check(lib().ddm_b200_compare(str(path).encode(), f, C.byref(c), ids[algorithms[0]], ids[algorithms[1]],
+                                  C.byref(dev), C.byref(tol), C.byref(ok), C.byref(ta), C.byref(tb)))
+    resolved = fmt if fmt != "auto" else ("pgm_dir" if os.path.isdir(path) else "raw_stack")
+    report = {"subcommand": "compare", "tool_version": "0.1.0-b200", "input": str(path),
+              "format": resolved, "algorithms": list(algorithms), "precision": config.precision,
+              "deviation": dev.value, "tolerance": tol.value, "pass": bool(ok.value)}
+    if out:
+        os.makedirs(out, exist_ok=True)
+        with open(os.path.join(out, "compare.json"), "w") as fh:
+            json.dump(report, fh, indent=2, sort_keys=True)
+            fh.write("\n")
+    report["timing"] = [{k: float(getattr(t, k)) for k, _ in Timing._fields_} for t in (ta, tb)]
+    return report
+
+
+def synth(out: str, size: int = 64, frames: int = 256, particles: int = 100, diffusion: float = 0.5,
+          psf_sigma: float = 1.0, amplitude: float = 1000.0, background: float = 100.0,
+          frame_interval: float = 1.0, seed: int = 0) -> str:
+    """`ddm synth` (`tools/ddm_cli.cpp:306-327`): out/stack.raw + out/synth.json. Returns the
+    stack path."""
+    _check(lib().ddm_b200_synth(str(out).encode(), C.c_int64(particles), C.c_double(diffusion),
+                                C.c_double(psf_sigma), C.c_double(amplitude), C.c_double(background),
+                                int(size), int(frames), C.c_double(frame_interval), C.c_uint64(seed)))
+    return os.path.join(out, "stack.raw")
+
+
 @dataclass
 class LagProfile:
     d: np.ndarray

@@ -158,3 +158,23 @@ def test_stale_partials_in_out_dir_fail_as_the_reference(ddm, tmp_path):
     (out / "partials" / "group9.bin").write_bytes(b"not a partial\n")
     with pytest.raises(ddm.InputError):
         ddm.run(st, ddm.RunConfig(memory_bytes=1 << 40, out_dir=str(out)))
+
+
+# ----------------------------------------------------------------- `ddm compare`
+
+@pytest.mark.parametrize("prec, algs", [("f64", ("with_ft", "without_ft")), ("f32", ("with_ft", "without_ft")),
+                                        ("f64", ("with_ft", "direct"))])
+def test_compare_agrees_with_its_own_runs(ddm, tmp_path, prec, algs):
+    """`ddm compare` (`ddm_cli.cpp:247-290`): the deviation is max|a-b| / max(|a|,|b|) of the
+    two algorithms' maps (`:132-141`), within the CLI's tolerance; the reference's own pair of
+    runs on the same stack deviates within the same tolerance."""
+    path = ddm.synth(str(tmp_path / "s"), size=32, frames=48, particles=20, seed=3)
+    cfg = ddm.RunConfig(precision=prec, memory_bytes=1 << 40)
+    rep = ddm.compare(path, cfg, algorithms=algs, out=str(tmp_path / "o"))
+    maps = [ddm.run_raw_stack(path, ddm.RunConfig(algorithm=a, precision=prec, memory_bytes=1 << 40)).values
+            for a in algs]
+    peak = max(np.abs(maps[0]).max(), np.abs(maps[1]).max())
+    assert rep["deviation"] == pytest.approx(np.abs(maps[0] - maps[1]).max() / peak, rel=1e-12, abs=0)
+    assert rep["tolerance"] == (1e-4 if prec == "f32" else 1e-9) and rep["pass"]
+    saved = json.loads((tmp_path / "o" / "compare.json").read_text())
+    assert saved["pass"] and saved["algorithms"] == list(algs) and saved["deviation"] == rep["deviation"]

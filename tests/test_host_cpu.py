@@ -30,3 +30,34 @@ def test_analyze_missing_input_is_io_error(tmp_path):
         ddm.analyze(str(tmp_path / "none.raw"), str(tmp_path / "o"), ddm.RunConfig(), fmt="raw_stack")
     with pytest.raises(ddm.InputError):
         ddm.analyze(str(tmp_path), str(tmp_path / "o"), ddm.RunConfig(), fmt="tiff")
+
+
+def test_synth_writes_the_generated_stack_and_manifest(tmp_path):
+    """`ddm synth` (`ddm_cli.cpp:306-327`): stack.raw holds ddm::generate's frames (bit-identical
+    to the reference generator, tests/golden/synth.npz pins that) behind the raw-stack header;
+    synth.json echoes every SynthConfig field (`synth.cpp:134-155`)."""
+    import json
+    import numpy as np
+    path = ddm.synth(str(tmp_path / "s"), size=24, frames=10, particles=7, diffusion=0.3,
+                     frame_interval=0.5, seed=11)
+    st = ddm.load_stack(path, "raw_stack")
+    assert np.array_equal(st, ddm.generate(24, 24, 10, particles=7, diffusion=0.3, frame_interval=0.5, seed=11))
+    with open(path, "rb") as f:
+        hdr = json.loads(f.readline())
+    assert hdr == {"width": 24, "height": 24, "frames": 10, "dtype": "u16le", "frame_interval": 0.5}
+    man = json.loads((tmp_path / "s" / "synth.json").read_text())
+    assert man == {"tool_version": "0.1.0-b200", "generator": "mt19937_64/box-muller", "particles": 7,
+                   "diffusion": 0.3, "psf_sigma": 1.0, "amplitude": 1000.0, "background": 100.0,
+                   "width": 24, "height": 24, "frames": 10, "frame_interval": 0.5, "seed": 11}
+
+
+def test_synth_rejects_bad_config(tmp_path):
+    with pytest.raises(ddm.InputError):
+        ddm.synth(str(tmp_path / "s"), size=0)
+
+
+def test_compare_needs_two_known_algorithms(tmp_path):
+    with pytest.raises(ddm.InputError):
+        ddm.compare("x.raw", ddm.RunConfig(), algorithms=("with_ft",))
+    with pytest.raises(ddm.InputError):
+        ddm.compare("x.raw", ddm.RunConfig(), algorithms=("with_ft", "fast"))
