@@ -87,27 +87,17 @@ constexpr int kXP = 34;
 constexpr int kXS = 32 * kXP;
 
 // Length-1024 transform of the warp (lane a holds x[a + 32 b] in v[b]; on return lane c
-// holds X[c + 32 d] in v[d]).  Four-step twiddles come from a CTA table twt[a * kXP + c]
-// (lane-major, 128-bit loads): W_1024^{a c}, or for ODD W_2048^{a (2c + 1)}, where the input
-// is x[n] W_2048^{n}: its W_64^{b} part is applied before the register DFT and its lane factor
-// W_2048^{a} is folded into the table, so X = the odd outputs of the zero-padded FFT_2048.
+// holds X[c + 32 d] in v[d]).  Four-step: DFT_32 over b, exchange, then DFT_32 over a of
+// Y[a][c] W(a, c) with the twiddles fused into its first butterflies; lane c reads W(., c)
+// from row c of a CTA table twt[c * kXP + a] (128-bit loads): W_1024^{a c}, or for ODD
+// W_2048^{a (2c + 1)}, where the input is x[n] W_2048^{n}: its W_64^{b} part is applied
+// before the first DFT_32 and its lane factor W_2048^{a} is folded into the table, so X =
+// the odd outputs of the zero-padded FFT_2048.  W(0, c) = 1.
 template <int SIGN, bool ODD>
 __device__ __forceinline__ void fft1024(cpx<float> (&v)[32], cpx<float>* scratch, int lane,
                                         const cpx<float>* __restrict__ twt) {
     if constexpr (ODD) premul_w64<SIGN>(v);
     RegDft<32, SIGN, float>::run(v);
-    const float4* tw4 = reinterpret_cast<const float4*>(twt + lane * kXP);
-#pragma unroll
-    for (int c = 0; c < 32; c += 2) {
-        const float4 t = tw4[c / 2];
-        cpx<float> w0 = {t.x, t.y}, w1 = {t.z, t.w};
-        if (SIGN > 0) {
-            w0.y = -w0.y;
-            w1.y = -w1.y;
-        }
-        if (ODD || c > 0) v[c] = cmul(v[c], w0);
-        v[c + 1] = cmul(v[c + 1], w1);
-    }
 #pragma unroll
     for (int c = 0; c < 32; ++c) scratch[c * kXP + lane] = v[c];
     __syncwarp();
@@ -119,20 +109,27 @@ __device__ __forceinline__ void fft1024(cpx<float> (&v)[32], cpx<float>* scratch
         v[ap + 1] = {t.z, t.w};
     }
     __syncwarp();
-    RegDft<32, SIGN, float>::run(v);
+    const cpx<float>* tw = twt + lane * kXP;
+    auto twf = [tw](int a) {
+        cpx<float> w = tw[a];
+        if (SIGN > 0) w.y = -w.y;
+        return w;
+    };
+    dft32_fused<SIGN, float, true>(v, twf);
 }
 
-// Twiddle tables of fft1024 (kXS complex each): even W_1024^{a c}, odd W_2048^{a (2c + 1)}
+// Twiddle tables of fft1024 (kXS complex each), row c = lane c: even W_1024^{a c}, odd
+// W_2048^{a (2c + 1)}
 __device__ __forceinline__ void fill_fft1024_tables(cpx<float>* tw_even, cpx<float>* tw_odd,
                                                     int tid, int nthreads) {
     for (int i = tid; i < 32 * 32; i += nthreads) {
         const int a = i >> 5, c = i & 31;
         double sn, cs;
         sincospi(-2.0 * (double)(a * c) / 1024, &sn, &cs);
-        tw_even[a * kXP + c] = {(float)cs, (float)sn};
+        tw_even[a * kXP + c] = {(float)cs, (float)sn};   // symmetric in (a, c)
         if (tw_odd) {
             sincospi(-2.0 * (double)(a * (2 * c + 1)) / 2048, &sn, &cs);
-            tw_odd[a * kXP + c] = {(float)cs, (float)sn};
+            tw_odd[c * kXP + a] = {(float)cs, (float)sn};  // row c: the lane that applies it
         }
     }
 }

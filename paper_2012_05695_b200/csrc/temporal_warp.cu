@@ -66,7 +66,7 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
     extern __shared__ __align__(128) unsigned char smem_raw[];
     WarpSmem* ws = reinterpret_cast<WarpSmem*>(smem_raw);
     cpx<float>* tw_even = reinterpret_cast<cpx<float>*>(ws + kWarps);  // [a][c] W_1024^{a c}
-    cpx<float>* tw_odd = tw_even + kXS;                                  // [a][c] W_2048^{a (2c+1)}
+    cpx<float>* tw_odd = tw_even + kXS;                                  // [c][a] W_2048^{a (2c+1)}
     float* rcp = reinterpret_cast<float*>(tw_odd + kXS);                 // 1 / (N - m)
     float* acc_base = rcp + kL;                                          // kRing: [warp][kPad]
 

@@ -105,6 +105,61 @@ __device__ __forceinline__ void dft_composite(cpx<S>* v) {
     }
 }
 
+// DFT_32 as 4 x 8 with the inner twiddles fused into the row DFT_4's first butterflies:
+// b0 = y0 + w2 y2 (FMA chains), b1 = 2 y0 - b0, p = w1 y1, b2 = p + w3 y3, b3 = 2 p - b2
+// (24 instructions per row instead of 28; W_32^8 = SIGN i is a rotation).
+// TW: the input is v[n] tw(n) with tw(n) = twf(n) (a functor; tw(0) = 1 is skipped), fused
+// into the first butterflies of the column DFT_8s
+template <int SIGN, typename S, bool TW = false, class Tw = int>
+__device__ __forceinline__ void dft32_fused(cpx<S>* v, const Tw& twf = 0) {
+    cpx<S> y[4][8];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+#pragma unroll
+        for (int b = 0; b < 8; ++b) y[a][b] = v[a + 4 * b];
+        if constexpr (TW) {
+            // even b (n = a + 8 j) and odd b (n = a + 4 + 8 j) DFT_4s with the input twiddles
+            if (a == 0)
+                dft4_tw<SIGN>(y[a][0], y[a][2], y[a][4], y[a][6], twf(8), twf(16), twf(24));
+            else
+                dft4_tw<SIGN>(y[a][0], y[a][2], y[a][4], y[a][6], twf(a), twf(a + 8), twf(a + 16),
+                              twf(a + 24));
+            dft4_tw<SIGN>(y[a][1], y[a][3], y[a][5], y[a][7], twf(a + 4), twf(a + 12), twf(a + 20),
+                          twf(a + 28));
+            dft8_finish<SIGN>(y[a]);
+        } else {
+            Dft<8, SIGN, S>::run(y[a]);
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        cpx<S> b0, b1, b2, b3;
+        if (c == 0) {
+            b0 = cadd(y[0][0], y[2][0]);
+            b1 = csub(y[0][0], y[2][0]);
+            b2 = cadd(y[1][0], y[3][0]);
+            b3 = csub(y[1][0], y[3][0]);
+        } else {
+            if (c == 4) {
+                const cpx<S> t = rot90<SIGN>(y[2][c]);  // W_32^8
+                b0 = cadd(y[0][c], t);
+                b1 = csub(y[0][c], t);
+            } else {
+                b0 = cfma(ct_w<SIGN, S>(2 * c, 32), y[2][c], y[0][c]);
+                b1 = creflect(y[0][c], b0);
+            }
+            const cpx<S> p = cmul(y[1][c], ct_w<SIGN, S>(c, 32));
+            b2 = cfma(ct_w<SIGN, S>(3 * c, 32), y[3][c], p);
+            b3 = creflect(p, b2);
+        }
+        b3 = rot90<SIGN>(b3);
+        v[c] = cadd(b0, b2);
+        v[c + 16] = csub(b0, b2);
+        v[c + 8] = cadd(b1, b3);
+        v[c + 24] = csub(b1, b3);
+    }
+}
+
 template <int R, int SIGN, typename S>
 struct RegDft {
     __device__ __forceinline__ static void run(cpx<S>* v) {
@@ -112,7 +167,7 @@ struct RegDft {
         } else if constexpr (R <= 16) {
             Dft<R, SIGN, S>::run(v);
         } else if constexpr (R == 32) {
-            dft_composite<4, 8, SIGN, S>(v);
+            dft32_fused<SIGN, S>(v);
         } else if constexpr (R == 64) {
             dft_composite<8, 8, SIGN, S>(v);
         } else {

@@ -17,7 +17,8 @@ from typing import Callable, Optional, Sequence
 
 import numpy as np
 
-LIB_PATH = Path(__file__).resolve().parent / "libddm_b200.so"
+# DDM_B200_LIB: another build of the library (A/B timing of kernel variants); default in-tree
+LIB_PATH = Path(os.environ.get("DDM_B200_LIB") or Path(__file__).resolve().parent / "libddm_b200.so")
 
 
 class Error(RuntimeError):
