@@ -207,6 +207,8 @@ int64_t max_frames(bool f64);
 // Device reduction over n doubles: all finite?, max, min (for ResultArchive::validate).
 void reduce_stats(const double* d, int64_t n, cudaStream_t stream, bool* finite, double* max_v,
                   double* min_v);
+void reduce_stats(const float* d, int64_t n, cudaStream_t stream, bool* finite, double* max_v,
+                  double* min_v);
 
 // Deterministic ring average on device (`analysis.cpp:61-97`): values [L][plane] f64 device,
 // bins [plane] int32 (-1 = not retained), order/offsets = retained positions sorted by bin

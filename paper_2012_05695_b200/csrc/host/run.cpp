@@ -16,6 +16,7 @@
 #include "run_internal.hpp"
 
 #include <algorithm>
+#include <barrier>
 #include <atomic>
 #include <chrono>
 #include <cstdlib>
@@ -353,23 +354,38 @@ ResultArchive run_core(const Ingest& in, const RunConfig& config, double* out,
         }
         archive.map.values.clear();
     } else {
-        double* d_map = static_cast<double*>(eng.buffer("map", std::size_t(total) * sizeof(double)));
+        // DDM_D2H_WIDEN=1 (f32 runs): the map stays f32 on the device and is widened on the
+        // host while it streams back (exact; half the PCIe bytes). Opt-in: on the measured
+        // box 16 host threads widen at ~67 GB/s, about the PCIe rate, so the C2 e2e moved
+        // 32.2 -> 31.5 ms in one A/B round and regressed in the other.
+        static const char* widen_env = std::getenv("DDM_D2H_WIDEN");
+        const bool widen = !f64 && total >= (std::int64_t(1) << 22) && widen_env && widen_env[0] == '1';
+        const std::size_t eb = widen ? sizeof(float) : sizeof(double);
+        void* d_map = eng.buffer(widen ? "map32" : "map", std::size_t(total) * eb);
         if (!spec.identity)
-            b200::check(cudaMemsetAsync(d_map, 0, std::size_t(total) * sizeof(double), st), "memset");
+            b200::check(cudaMemsetAsync(d_map, 0, std::size_t(total) * eb, st), "memset");
         spec.d_out = d_map;
+        spec.out_f64 = !widen;
         eng.run(spec, &times);
         // validate on the device before the copy (`archive.cpp:44-58`)
         bool finite = true;
         double peak = 0.0, lowest = 0.0;
-        b200::reduce_stats(d_map, total, st, &finite, &peak, &lowest);
+        if (widen)
+            b200::reduce_stats(static_cast<const float*>(d_map), total, st, &finite, &peak, &lowest);
+        else
+            b200::reduce_stats(static_cast<const double*>(d_map), total, st, &finite, &peak, &lowest);
         if (!finite) throw InputError("result map contains non-finite values");
         const double eps = f64 ? 1e-9 : 1e-4;
         if (lowest < -eps * std::max(peak, 1.0))
             throw InputError("result map contains negative values beyond tolerance");
         clock.start();
-        b200::check(cudaMemcpyAsync(out, d_map, std::size_t(total) * sizeof(double),
-                                    cudaMemcpyDeviceToHost, st), "map copy");
-        b200::check(cudaStreamSynchronize(st), "sync");
+        if (widen) {
+            download_widen(eng, out, static_cast<const float*>(d_map), std::size_t(total), st);
+        } else {
+            b200::check(cudaMemcpyAsync(out, d_map, std::size_t(total) * sizeof(double),
+                                        cudaMemcpyDeviceToHost, st), "map copy");
+            b200::check(cudaStreamSynchronize(st), "sync");
+        }
         clock.stop(timing.merge);
     }
     timing.step1 = times.spatial_ms * 1e-3;
@@ -413,6 +429,46 @@ void upload_pageable(b200::Engine& eng, void* dst, const void* src, std::size_t 
         throw;
     }
     for (auto e : done) cudaEventDestroy(e);
+}
+
+void download_widen(b200::Engine& eng, double* out, const float* d, std::size_t n, cudaStream_t stream) {
+    constexpr std::size_t kChunk = std::size_t(4) << 20;  // values (16 MiB of f32) per slot
+    const std::size_t chunks = (n + kChunk - 1) / kChunk;
+    if (chunks == 0) return;
+    float* pin[2] = {static_cast<float*>(eng.pinned(0, kChunk * sizeof(float))),
+                     static_cast<float*>(eng.pinned(1, kChunk * sizeof(float)))};
+    cudaEvent_t ev[2];
+    for (auto& e : ev) b200::check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    cudaError_t err = cudaSuccess;
+    auto issue = [&](std::size_t i) {
+        const std::size_t off = i * kChunk, m = std::min(kChunk, n - off);
+        if (err == cudaSuccess) err = cudaMemcpyAsync(pin[i & 1], d + off, m * sizeof(float), cudaMemcpyDeviceToHost, stream);
+        if (err == cudaSuccess) err = cudaEventRecord(ev[i & 1], stream);
+    };
+    issue(0);
+    if (chunks > 1) issue(1);
+    const unsigned T = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    std::barrier sync(std::ptrdiff_t(T), [] () noexcept {});
+    auto worker = [&](unsigned t) {
+        for (std::size_t i = 0; i < chunks; ++i) {
+            if (t == 0 && err == cudaSuccess) err = cudaEventSynchronize(ev[i & 1]);
+            sync.arrive_and_wait();  // chunk i is in slot i & 1
+            const std::size_t off = i * kChunk, m = std::min(kChunk, n - off);
+            const std::size_t b = m * t / T, e = m * (t + 1) / T;
+            const float* src = pin[i & 1];
+            double* dst = out + off;
+            for (std::size_t k = b; k < e; ++k) dst[k] = double(src[k]);
+            sync.arrive_and_wait();  // slot i & 1 is free again
+            if (t == 0 && i + 2 < chunks) issue(i + 2);
+        }
+    };
+    std::vector<std::thread> pool;
+    for (unsigned t = 1; t < T; ++t) pool.emplace_back(worker, t);
+    worker(0);
+    for (auto& th : pool) th.join();
+    cudaStreamSynchronize(stream);
+    for (auto e : ev) cudaEventDestroy(e);
+    b200::check(err, "map download");
 }
 
 }  // namespace detail

@@ -71,6 +71,11 @@ void parallel_for(std::size_t n, Fn&& fn) {
 void upload_pageable(b200::Engine& eng, void* dst, const void* src, std::size_t bytes,
                      cudaStream_t stream);
 
+// Device f32 -> host f64 (exact widening): chunks of the f32 map stream through the engine's
+// two pinned slots while host threads widen the previous chunk into `out`, so PCIe carries
+// 4 bytes per value instead of 8. Caller holds the engine lock.
+void download_widen(b200::Engine& eng, double* out, const float* d, std::size_t n, cudaStream_t stream);
+
 // DDM_TRACE=1: wall time of each host phase on stderr ("[tag] phase ms")
 struct Trace {
     const char* tag;

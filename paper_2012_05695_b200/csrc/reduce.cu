@@ -13,11 +13,12 @@ namespace ddm::b200 {
 
 namespace {
 
-__global__ void stats_kernel(const double* __restrict__ d, int64_t n, double* __restrict__ part) {
+template <typename T>
+__global__ void stats_kernel(const T* __restrict__ d, int64_t n, double* __restrict__ part) {
     double mx = -DBL_MAX, mn = DBL_MAX, bad = 0.0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
-        const double v = d[i];
+        const double v = (double)d[i];
         if (!isfinite(v)) bad = 1.0;
         else {
             mx = fmax(mx, v);
@@ -63,13 +64,14 @@ __global__ void radial_kernel(const double* __restrict__ values, int64_t n_lags,
 
 }  // namespace
 
-void reduce_stats(const double* d, int64_t n, cudaStream_t stream, bool* finite, double* max_v,
-                  double* min_v) {
+template <typename T>
+static void reduce_stats_t(const T* d, int64_t n, cudaStream_t stream, bool* finite, double* max_v,
+                           double* min_v) {
     const int blocks = 296, threads = 256;
     double* part = nullptr;
     check(cudaMallocAsync(reinterpret_cast<void**>(&part), sizeof(double) * 3 * blocks, stream),
           "cudaMallocAsync");
-    stats_kernel<<<blocks, threads, 0, stream>>>(d, n, part);
+    stats_kernel<T><<<blocks, threads, 0, stream>>>(d, n, part);
     check(cudaGetLastError(), "stats kernel");
     double host[3 * 296];
     check(cudaMemcpyAsync(host, part, sizeof(host), cudaMemcpyDeviceToHost, stream), "stats copy");
@@ -84,6 +86,15 @@ void reduce_stats(const double* d, int64_t n, cudaStream_t stream, bool* finite,
     *finite = bad == 0.0;
     *max_v = n > 0 ? mx : 0.0;
     *min_v = n > 0 ? mn : 0.0;
+}
+
+void reduce_stats(const double* d, int64_t n, cudaStream_t stream, bool* finite, double* max_v,
+                  double* min_v) {
+    reduce_stats_t(d, n, stream, finite, max_v, min_v);
+}
+void reduce_stats(const float* d, int64_t n, cudaStream_t stream, bool* finite, double* max_v,
+                  double* min_v) {
+    reduce_stats_t(d, n, stream, finite, max_v, min_v);
 }
 
 void radial_means(const double* d_values, int64_t n_lags, int64_t plane, const int64_t* d_order,
