@@ -210,6 +210,11 @@ void* Engine::buffer(const std::string& name, size_t bytes) {
     return b->ensure(bytes);
 }
 
+bool f32_register_temporal(int N) {
+    const int N2 = (int)pad_len(N);
+    return use_warp_temporal(N, N2, 8) || use_long_temporal(N, N2, 8);
+}
+
 int64_t max_frames(bool f64) {
     int64_t best = 0;
     for (int64_t n = 1; n <= (1 << 15); n <<= 1)

@@ -203,6 +203,9 @@ public:
 
 // Hardware limits of the one-CTA temporal kernel (longest supported sequence).
 int64_t max_frames(bool f64);
+// true when an f32 WITH_FT run of N frames uses a register temporal engine (warp or long),
+// which computes d(q, m) in f32: its map is exactly representable as f32
+bool f32_register_temporal(int N);
 
 // Device reduction over n doubles: all finite?, max, min (for ResultArchive::validate).
 void reduce_stats(const double* d, int64_t n, cudaStream_t stream, bool* finite, double* max_v,

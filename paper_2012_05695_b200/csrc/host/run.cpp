@@ -359,7 +359,8 @@ ResultArchive run_core(const Ingest& in, const RunConfig& config, double* out,
         // box 16 host threads widen at ~67 GB/s, about the PCIe rate, so the C2 e2e moved
         // 32.2 -> 31.5 ms in one A/B round and regressed in the other.
         static const char* widen_env = std::getenv("DDM_D2H_WIDEN");
-        const bool widen = !f64 && total >= (std::int64_t(1) << 22) && widen_env && widen_env[0] == '1';
+        const bool widen = !f64 && total >= (std::int64_t(1) << 22) && widen_env && widen_env[0] == '1' &&
+                           b200::f32_register_temporal(N);
         const std::size_t eb = widen ? sizeof(float) : sizeof(double);
         void* d_map = eng.buffer(widen ? "map32" : "map", std::size_t(total) * eb);
         if (!spec.identity)

@@ -178,3 +178,22 @@ def test_compare_agrees_with_its_own_runs(ddm, tmp_path, prec, algs):
     assert rep["tolerance"] == (1e-4 if prec == "f32" else 1e-9) and rep["pass"]
     saved = json.loads((tmp_path / "o" / "compare.json").read_text())
     assert saved["pass"] and saved["algorithms"] == list(algs) and saved["deviation"] == rep["deviation"]
+
+
+def test_widened_f32_download_is_bit_identical(ddm, tmp_path):
+    """DDM_D2H_WIDEN=1: the f32 device map widened on the host (exact) equals the f64 device
+    map path bit for bit where the temporal engine computes d in f32 (the register engines,
+    N = 1024 here; a map above the 4 M-value threshold)."""
+    import subprocess
+    import sys
+    st = ddm.generate(128, 64, 1024, particles=40, seed=9)
+    np.save(tmp_path / "st.npy", st)
+    code = ("import numpy as np, sys; sys.path.insert(0, '.'); from paper_2012_05695_b200 import ddm; "
+            f"st = np.load('{tmp_path}/st.npy'); a = ddm.run(st, ddm.RunConfig(precision='f32', memory_bytes=1 << 40)); "
+            f"np.save('{tmp_path}/w.npy', a.values)")
+    root = Path(__file__).resolve().parents[1]
+    env = dict(__import__("os").environ, DDM_D2H_WIDEN="1")
+    subprocess.run([sys.executable, "-c", code], cwd=root, env=env, check=True, timeout=300)
+    ref = ddm.run(st, ddm.RunConfig(precision="f32", memory_bytes=1 << 40)).values
+    assert ref.size >= 1 << 22
+    assert np.array_equal(np.load(tmp_path / "w.npy"), ref)
