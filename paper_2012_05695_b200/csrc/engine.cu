@@ -768,12 +768,15 @@ void Engine::run_pairwise(const RunSpec& sp, PhaseTimes* times) {
         d_dest = static_cast<const int64_t*>(dest_.get());
     }
     if (times) check(cudaEventRecord(ev_[2], stream_), "cudaEventRecord");
+    int lag0 = lags.empty() ? -1 : lags[0];   // contiguous lag range -> windowed kernel
+    for (size_t i = 1; i < lags.size() && lag0 >= 0; ++i)
+        if (lags[i] != lags[0] + (int)i) lag0 = -1;
     check(sp.f64 ? ddmk::launch_pairwise<double>(d_spec, N, count, d_lags, (int)lags.size(),
                                                  static_cast<double*>(sp.d_out), sp.out_stride, d_dest,
-                                                 num_sms_, stream_)
+                                                 num_sms_, stream_, lag0)
                  : ddmk::launch_pairwise<float>(d_spec, N, count, d_lags, (int)lags.size(),
                                                 static_cast<double*>(sp.d_out), sp.out_stride, d_dest,
-                                                num_sms_, stream_),
+                                                num_sms_, stream_, lag0),
           "pairwise kernel");
     if (times) check(cudaEventRecord(ev_[3], stream_), "cudaEventRecord");
     check(cudaStreamSynchronize(stream_), "sync");   // host lag / slot vectors

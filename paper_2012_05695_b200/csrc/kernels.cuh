@@ -110,9 +110,11 @@ cudaError_t launch_ring_means(const double* partial, int N, const int* lag_index
 // WITHOUT_FT (`pairwise.cpp:11-72`): spec wave-vector-major [q][N] in the working precision,
 // lags ascending (n_lags entries, 0 allowed), out[li * out_stride + dest(q)] f64.
 template <typename S>
+// lag0 >= 0: the lags are the contiguous range [lag0, lag0 + n_lags) (the common "all lags"
+// request), served by the register-windowed kernel; lag0 < 0: any ascending list
 cudaError_t launch_pairwise(const void* spec, int N, int64_t nq, const int* lags, int n_lags,
                             double* out, int64_t out_stride, const int64_t* dest_of_slot,
-                            int num_sms, cudaStream_t stream);
+                            int num_sms, cudaStream_t stream, int lag0 = -1);
 
 // Relaxation fits, one warp per ring (`analysis.cpp:108-224`): means [n_lags][nbins] f64;
 // flag 0 ok, 1 degenerate, 2 no_converge, -1 not fitted.

@@ -13,6 +13,7 @@
 // widened to f64 in shared memory once; each warp takes 32 consecutive requested lags, lane
 // l owns lag m_l and walks n upward, reading S_n (a broadcast) and S_{n - m_l}.
 #include <algorithm>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -53,12 +54,107 @@ pairwise_kernel(const cpx<S>* __restrict__ spec, int N, int64_t nq, const int* _
     }
 }
 
+// Contiguous lag range: lane l of a group owns lags L = base + kLpl l + k (k < kLpl) and walks
+// its own n = L - k + t. The S_{n - L} operand is then s[t - k], the same for every lane:
+// one broadcast load per step feeds a kLpl-deep register ring, and the per-lane operand S_n
+// is one load shared by the lane's kLpl sums. Every (q, L) sum still runs over ascending n
+// with the reference's arithmetic (bit-identical to pairwise_kernel); shared traffic per
+// pair drops ~kLpl x, so the loop is FP64-bound. Lag groups of 32 kLpl are dealt to warps
+// in (g, G - 1 - g) pairs, which balances the N - L trip counts.
+constexpr int kLpl = 4;
+constexpr int kConsecThreads = 128;
+
+__device__ __forceinline__ int pad_idx(int i) { return i + i / kLpl; }   // breaks the kLpl stride
+
+__device__ __forceinline__ double pair_norm(double2 a, double2 b) {
+    const double re = __dsub_rn(a.x, b.x), im = __dsub_rn(a.y, b.y);
+    return __dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im));
+}
+
+template <typename S>
+__global__ void __launch_bounds__(kConsecThreads)
+pairwise_consec_kernel(const cpx<S>* __restrict__ spec, int N, int64_t nq, int lag0, int n_lags,
+                       double* __restrict__ out, int64_t out_stride,
+                       const int64_t* __restrict__ dest_of_slot) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double2* s = reinterpret_cast<double2*>(smem_raw);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+    constexpr int kGroup = 32 * kLpl;
+    const int groups = (n_lags + kGroup - 1) / kGroup;
+    const int pairs = (groups + 1) / 2;
+    for (int64_t q = blockIdx.x; q < nq; q += gridDim.x) {
+        __syncthreads();
+        const cpx<S>* src = spec + q * (int64_t)N;
+        for (int n = threadIdx.x; n < N; n += blockDim.x)
+            s[pad_idx(n)] = make_double2((double)src[n].x, (double)src[n].y);
+        __syncthreads();
+        const int64_t dst = dest_of_slot ? dest_of_slot[q] : q;
+        for (int p = warp; p < pairs; p += nwarps) {
+#pragma unroll 1
+            for (int side = 0; side < 2; ++side) {
+                const int g = side == 0 ? p : groups - 1 - p;
+                if (side == 1 && g == p) break;
+                const int base = lag0 + g * kGroup + kLpl * lane;   // this lane's first lag
+                double acc[kLpl];
+#pragma unroll
+                for (int k = 0; k < kLpl; ++k) acc[k] = 0.0;
+                double2 ring[kLpl];
+                // n = base + t; lag base + k is summed from t = k on
+#pragma unroll
+                for (int j = 0; j < kLpl; ++j) {
+                    const int n = base + j;
+                    if (n < N) {
+                        ring[j] = s[pad_idx(j)];
+                        const double2 b = s[pad_idx(n)];
+#pragma unroll
+                        for (int k = 0; k <= j; ++k) acc[k] = __dadd_rn(acc[k], pair_norm(ring[j - k], b));
+                    }
+                }
+                for (int t0 = kLpl; base + t0 < N; t0 += kLpl) {
+#pragma unroll
+                    for (int j = 0; j < kLpl; ++j) {
+                        const int t = t0 + j, n = base + t;
+                        if (n < N) {
+                            ring[j] = s[pad_idx(t)];
+                            const double2 b = s[pad_idx(n)];
+#pragma unroll
+                            for (int k = 0; k < kLpl; ++k)
+                                acc[k] = __dadd_rn(acc[k], pair_norm(ring[(j - k + kLpl) % kLpl], b));
+                        }
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < kLpl; ++k) {
+                    const int m = base + k, li = m - lag0;
+                    if (li < n_lags && m < N)
+                        out[(int64_t)li * out_stride + dst] = m == 0 ? 0.0 : acc[k] * (1.0 / (double)(N - m));
+                }
+            }
+        }
+    }
+}
+
 }  // namespace
 
 template <typename S>
 cudaError_t launch_pairwise(const void* spec, int N, int64_t nq, const int* lags, int n_lags,
                             double* out, int64_t out_stride, const int64_t* dest_of_slot,
-                            int num_sms, cudaStream_t stream) {
+                            int num_sms, cudaStream_t stream, int lag0) {
+    static const bool generic = std::getenv("DDM_PAIRWISE_GENERIC") != nullptr;   // A/B
+    if (lag0 >= 0 && !generic) {
+        const size_t smem = (size_t)(N + N / kLpl + 1) * sizeof(double2);
+        if (smem > 227 * 1024) return cudaErrorInvalidValue;
+        auto k = pairwise_consec_kernel<S>;
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        int occ = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kConsecThreads, smem);
+        const int64_t grid = std::min<int64_t>(nq, (int64_t)std::max(1, occ) * num_sms * 4);
+        if (grid == 0) return cudaSuccess;
+        k<<<(unsigned)grid, kConsecThreads, smem, stream>>>(static_cast<const cpx<S>*>(spec), N, nq, lag0,
+                                                            n_lags, out, out_stride, dest_of_slot);
+        return cudaGetLastError();
+    }
     const size_t smem = (size_t)N * sizeof(double2);
     if (smem > 227 * 1024) return cudaErrorInvalidValue;
     auto k = pairwise_kernel<S>;
@@ -74,8 +170,8 @@ cudaError_t launch_pairwise(const void* spec, int N, int64_t nq, const int* lags
 }
 
 template cudaError_t launch_pairwise<float>(const void*, int, int64_t, const int*, int, double*,
-                                            int64_t, const int64_t*, int, cudaStream_t);
+                                            int64_t, const int64_t*, int, cudaStream_t, int);
 template cudaError_t launch_pairwise<double>(const void*, int, int64_t, const int*, int, double*,
-                                             int64_t, const int64_t*, int, cudaStream_t);
+                                             int64_t, const int64_t*, int, cudaStream_t, int);
 
 }  // namespace ddmk
