@@ -141,18 +141,23 @@ cudaError_t launch_pairwise(const void* spec, int N, int64_t nq, const int* lags
                             double* out, int64_t out_stride, const int64_t* dest_of_slot,
                             int num_sms, cudaStream_t stream, int lag0) {
     static const bool generic = std::getenv("DDM_PAIRWISE_GENERIC") != nullptr;   // A/B
-    if (lag0 >= 0 && !generic) {
+    // a contiguous range of at least one full lag group (32 lanes x kLpl lags): shorter ranges
+    // leave most lanes idle and stay on the one-lane-per-lag kernel
+    if (lag0 >= 0 && !generic && n_lags >= 32 * kLpl) {
         const size_t smem = (size_t)(N + N / kLpl + 1) * sizeof(double2);
         if (smem > 227 * 1024) return cudaErrorInvalidValue;
         auto k = pairwise_consec_kernel<S>;
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
+        // one warp per (g, G-1-g) group pair, at most kConsecThreads / 32 per CTA
+        const int pairs = ((n_lags + 32 * kLpl - 1) / (32 * kLpl) + 1) / 2;
+        const int threads = 32 * std::min(kConsecThreads / 32, std::max(1, pairs));
         int occ = 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kConsecThreads, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, threads, smem);
         const int64_t grid = std::min<int64_t>(nq, (int64_t)std::max(1, occ) * num_sms * 4);
         if (grid == 0) return cudaSuccess;
-        k<<<(unsigned)grid, kConsecThreads, smem, stream>>>(static_cast<const cpx<S>*>(spec), N, nq, lag0,
-                                                            n_lags, out, out_stride, dest_of_slot);
+        k<<<(unsigned)grid, threads, smem, stream>>>(static_cast<const cpx<S>*>(spec), N, nq, lag0, n_lags,
+                                                     out, out_stride, dest_of_slot);
         return cudaGetLastError();
     }
     const size_t smem = (size_t)N * sizeof(double2);
