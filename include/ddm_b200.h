@@ -135,6 +135,13 @@ int ddm_b200_compare(const char* path, int format, const ddm_b200_run_config* co
 int ddm_b200_synth(const char* out_dir, int64_t particles, double diffusion, double psf_sigma,
                    double amplitude, double background, int size, int frames, double frame_interval,
                    uint64_t seed);
+/* ddm::crossover (core/src/bench.cpp:144-183) over a table of n_cells cells (algorithm 0/1/2,
+   frames, square size, median total seconds, failed flag; failed may be NULL): per size in
+   first-seen order, the smallest N whose first with_ft cell beats the first without_ft cell
+   (-1 = none).  sizes_out / n_star_out need room for one entry per distinct size.  Host only. */
+int ddm_b200_crossover(int64_t n_cells, const int* algorithm, const int* frames, const int* width,
+                       const double* seconds_total, const int* failed, int* sizes_out, int* n_star_out,
+                       int* n_out);
 /* Dimensions of a stack on disk (format 0 raw_stack, 1 pgm_dir; open_frame_source). */
 int ddm_b200_stack_dims(const char* path, int format, int* width, int* height, int* frames);
 

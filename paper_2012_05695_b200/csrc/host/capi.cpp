@@ -323,6 +323,30 @@ int ddm_b200_synth(const char* out_dir, int64_t particles, double diffusion, dou
     });
 }
 
+int ddm_b200_crossover(int64_t n_cells, const int* algorithm, const int* frames, const int* width,
+                       const double* seconds_total, const int* failed, int* sizes_out, int* n_star_out,
+                       int* n_out) {
+    return guarded([&] {
+        if (n_cells < 0 || (n_cells > 0 && (!algorithm || !frames || !width || !seconds_total)))
+            throw ddm::InputError("null table");
+        std::vector<ddm::BenchCell> table(static_cast<std::size_t>(n_cells));
+        for (int64_t i = 0; i < n_cells; ++i) {
+            auto& c = table[std::size_t(i)];
+            c.algorithm = algorithm[i] == 0 ? "with_ft" : algorithm[i] == 1 ? "without_ft" : "direct";
+            c.frames = frames[i];
+            c.width = c.height = width[i];
+            c.seconds_total = seconds_total[i];
+            c.failed = failed && failed[i] != 0;
+        }
+        const auto xs = ddm::crossover(table);
+        if (n_out) *n_out = int(xs.size());
+        for (std::size_t i = 0; i < xs.size(); ++i) {
+            if (sizes_out) sizes_out[i] = xs[i].size;
+            if (n_star_out) n_star_out[i] = xs[i].n_star ? *xs[i].n_star : -1;
+        }
+    });
+}
+
 int ddm_b200_stack_dims(const char* path, int format, int* width, int* height, int* frames) {
     return guarded([&] {
         if (!path || !width || !height || !frames) throw ddm::InputError("null argument");

@@ -415,6 +415,23 @@ def compare(path: str, config: RunConfig, algorithms=("with_ft", "without_ft"), 
     return report
 
 
+def crossover(cells) -> dict:
+    """ddm::crossover (`core/src/bench.cpp:144-183`) on [(algorithm, N, size, seconds_total,
+    failed), ...]: {size: N* or None}."""
+    ids = {"with_ft": 0, "without_ft": 1, "direct": 2}
+    n = len(cells)
+    alg = np.asarray([ids[c[0]] for c in cells], np.int32)
+    fr = np.asarray([c[1] for c in cells], np.int32)
+    sz = np.asarray([c[2] for c in cells], np.int32)
+    tot = np.asarray([c[3] for c in cells], np.float64)
+    fail = np.asarray([1 if (len(c) > 4 and c[4]) else 0 for c in cells], np.int32)
+    out_s, out_n, cnt = np.zeros(max(n, 1), np.int32), np.zeros(max(n, 1), np.int32), C.c_int(0)
+    _check(lib().ddm_b200_crossover(C.c_int64(n), _p(alg, C.c_int), _p(fr, C.c_int), _p(sz, C.c_int),
+                                    _p(tot, C.c_double), _p(fail, C.c_int), _p(out_s, C.c_int),
+                                    _p(out_n, C.c_int), C.byref(cnt)))
+    return {int(out_s[i]): (int(out_n[i]) if out_n[i] >= 0 else None) for i in range(cnt.value)}
+
+
 def synth(out: str, size: int = 64, frames: int = 256, particles: int = 100, diffusion: float = 0.5,
           psf_sigma: float = 1.0, amplitude: float = 1000.0, background: float = 100.0,
           frame_interval: float = 1.0, seed: int = 0) -> str:

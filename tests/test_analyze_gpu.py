@@ -197,3 +197,21 @@ def test_widened_f32_download_is_bit_identical(ddm, tmp_path):
     ref = ddm.run(st, ddm.RunConfig(precision="f32", memory_bytes=1 << 40)).values
     assert ref.size >= 1 << 22
     assert np.array_equal(np.load(tmp_path / "w.npy"), ref)
+
+
+def test_bench_counters_scale_as_the_reference_expects(ddm):
+    """`test_bench.cpp:66-107`: WITHOUT_FT pairs N(N-1)/2, WITH_FT one group with two temporal
+    transforms per wave vector (8 x 5 at 8^2) and N spatial transforms; counters never
+    shrink as N grows."""
+    rows, _ = ddm.bench_sweep((8, 16, 32, 256, 512), (8,), repetitions=1, warmup=0)
+    cell = {(r["algorithm"], int(r["N"])): r for r in rows}
+    assert int(cell[("without_ft", 256)]["count_pairs"]) == 256 * 255 // 2
+    assert int(cell[("without_ft", 512)]["count_pairs"]) == 512 * 511 // 2
+    f = cell[("with_ft", 256)]
+    assert int(f["groups_or_passes"]) == 1 and int(f["count_temporal_ffts"]) == 2 * 8 * 5
+    assert int(f["count_spatial_ffts"]) == 256
+    for alg in ("with_ft", "without_ft"):
+        sp = [int(cell[(alg, n)]["count_spatial_ffts"]) for n in (8, 16, 32, 256, 512)]
+        pr = [int(cell[(alg, n)]["count_pairs"]) for n in (8, 16, 32, 256, 512)]
+        assert sp == sorted(sp) and pr == sorted(pr)
+        assert all(float(cell[(alg, n)]["seconds_total"]) > 0 for n in (8, 16, 32, 256, 512))

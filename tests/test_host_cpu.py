@@ -61,3 +61,21 @@ def test_compare_needs_two_known_algorithms(tmp_path):
         ddm.compare("x.raw", ddm.RunConfig(), algorithms=("with_ft",))
     with pytest.raises(ddm.InputError):
         ddm.compare("x.raw", ddm.RunConfig(), algorithms=("with_ft", "fast"))
+
+
+def test_crossover_reports_the_first_frame_count_that_wins():
+    """`test_bench.cpp:109-128`: N* is the first N whose with_ft total beats without_ft's;
+    a size where it never does reports none; sizes in first-seen order."""
+    cells = [("with_ft", 256, 32, 5.0), ("without_ft", 256, 32, 1.0),
+             ("with_ft", 512, 32, 3.0), ("without_ft", 512, 32, 2.5),
+             ("with_ft", 1024, 32, 2.0), ("without_ft", 1024, 32, 4.0),
+             ("with_ft", 256, 64, 9.0), ("without_ft", 256, 64, 1.0)]
+    assert list(ddm.crossover(cells).items()) == [(32, 1024), (64, None)]
+
+
+def test_crossover_skips_failed_cells():
+    """Failed cells (a plan that did not fit) never win or lose (`bench.cpp:158-166`)."""
+    cells = [("with_ft", 64, 16, 1.0, True), ("without_ft", 64, 16, 2.0),
+             ("with_ft", 128, 16, 1.0), ("without_ft", 128, 16, 2.0)]
+    assert ddm.crossover(cells) == {16: 128}
+    assert ddm.crossover([]) == {}
