@@ -1,0 +1,25 @@
+"""The reference-named C++ API (include/ddm/*.hpp) as a C++ caller uses it: host-only drivers
+under tests/cpp/ are compiled against include/ and linked with libddm_b200.so, then run
+(CPU; they make no device calls)."""
+import shutil
+import subprocess
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+LIB_DIR = ROOT / "paper_2012_05695_b200"
+
+
+@pytest.mark.parametrize("name", ["archive_api", "analysis_api"])
+def test_cpp_driver(tmp_path, name):
+    cxx = shutil.which("g++") or shutil.which("c++")
+    if cxx is None or not (LIB_DIR / "libddm_b200.so").exists():
+        pytest.skip("no C++ compiler or library not built")
+    exe = tmp_path / name
+    subprocess.run([cxx, "-std=c++20", "-O1", f"-I{ROOT / 'include'}", str(ROOT / "tests" / "cpp" / f"{name}.cpp"),
+                    f"-L{LIB_DIR}", "-lddm_b200", f"-Wl,-rpath,{LIB_DIR}", "-o", str(exe)],
+                   check=True, capture_output=True, text=True, timeout=300)
+    r = subprocess.run([str(exe), str(tmp_path / "work")], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.strip().startswith("OK")
