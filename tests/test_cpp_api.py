@@ -11,8 +11,7 @@ ROOT = Path(__file__).resolve().parents[1]
 LIB_DIR = ROOT / "paper_2012_05695_b200"
 
 
-@pytest.mark.parametrize("name", ["archive_api", "analysis_api"])
-def test_cpp_driver(tmp_path, name):
+def _build_and_run(tmp_path, name):
     cxx = shutil.which("g++") or shutil.which("c++")
     if cxx is None or not (LIB_DIR / "libddm_b200.so").exists():
         pytest.skip("no C++ compiler or library not built")
@@ -23,3 +22,15 @@ def test_cpp_driver(tmp_path, name):
     r = subprocess.run([str(exe), str(tmp_path / "work")], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert r.stdout.strip().startswith("OK")
+
+
+@pytest.mark.parametrize("name", ["archive_api", "analysis_api"])
+def test_cpp_driver(tmp_path, name):
+    _build_and_run(tmp_path, name)
+
+
+@pytest.mark.gpu
+def test_cpp_run_api_on_device(tmp_path):
+    """INTEGRATION.md §1: a C++ program compiled against include/ddm/*.hpp runs ddm::run,
+    ddm::compare and ddm::analyze on the B200 through libddm_b200.so."""
+    _build_and_run(tmp_path, "run_api")
