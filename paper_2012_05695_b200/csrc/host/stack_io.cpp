@@ -6,6 +6,7 @@
 #include "json_lite.hpp"
 
 #include <algorithm>
+#include <cstdio>
 #include <cctype>
 #include <cstring>
 #include <fstream>
@@ -98,6 +99,7 @@ ImageStack load_stack(const fs::path& path, StackFormat format) {
 }
 
 void write_raw_stack(const ImageStack& stack, const fs::path& path) {
+    // one JSON header line, then the samples as u16 little-endian (`image_stack.cpp:223-247`)
     stack.validate();
     json::Value h = json::Value::object();
     h.obj["width"] = json::Value::integer(stack.width);
@@ -105,16 +107,19 @@ void write_raw_stack(const ImageStack& stack, const fs::path& path) {
     h.obj["frames"] = json::Value::integer(stack.frames);
     h.obj["dtype"] = json::Value::string("u16le");
     h.obj["frame_interval"] = json::Value::number(stack.frame_interval);
-    std::ofstream out(path, std::ios::binary | std::ios::trunc);
-    if (!out) throw IoError("cannot open " + path.string() + " for writing");
-    out << json::dump(h) << '\n';
-    std::vector<unsigned char> raw(stack.pixels.size() * 2);
-    for (std::size_t i = 0; i < stack.pixels.size(); ++i) {
-        raw[2 * i] = (unsigned char)(stack.pixels[i] & 0xFF);
-        raw[2 * i + 1] = (unsigned char)(stack.pixels[i] >> 8);
+    std::string bytes = json::dump(h);
+    bytes.push_back('\n');
+    const std::size_t head = bytes.size();
+    bytes.resize(head + 2 * stack.pixels.size());
+    unsigned char* dst = reinterpret_cast<unsigned char*>(bytes.data()) + head;
+    for (const std::uint16_t px : stack.pixels) {   // explicit LE, whatever the host order
+        *dst++ = static_cast<unsigned char>(px);
+        *dst++ = static_cast<unsigned char>(px >> 8);
     }
-    out.write(reinterpret_cast<const char*>(raw.data()), std::streamsize(raw.size()));
-    if (!out) throw IoError("write failed for " + path.string());
+    std::FILE* f = std::fopen(path.c_str(), "wb");
+    if (!f) throw IoError("cannot open " + path.string() + " for writing");
+    const bool ok = std::fwrite(bytes.data(), 1, bytes.size(), f) == bytes.size();
+    if (std::fclose(f) != 0 || !ok) throw IoError("write failed for " + path.string());
 }
 
 MemoryFrameSource::MemoryFrameSource(ImageStack stack) : stack_(std::move(stack)) {
