@@ -118,10 +118,28 @@ def traffic_from_profiles(stage: str):
         vals = [v["dram_bytes"] for v in caps.values() if v["stage"] == stage]
         if not vals:
             return None
+        inst = [v.get("warp_inst") for v in caps.values() if v["stage"] == stage]
         return {"dram_bytes_per_launch": sum(vals), "capture": d["latest"],
-                "kernels": sorted(k for k, v in caps.items() if v["stage"] == stage)}
+                "kernels": sorted(k for k, v in caps.items() if v["stage"] == stage),
+                "warp_inst_per_launch": sum(inst) if all(i is not None for i in inst) else None}
     except Exception:
         return None
+
+
+def issue_view(tr, launch_ms, clocks):
+    """The dominant kernel's other ceiling: warp instructions per launch (ncu capture, fixed
+    by the code) / live launch time, against 4 issue slots per SM per clock (148 SMs at the
+    sampled SM clock). K3 is issue-bound, so this fraction, not HBM's, says how far it is from
+    its ceiling."""
+    if not tr or not tr.get("warp_inst_per_launch") or not launch_ms:
+        return None
+    mhz = (clocks or {}).get("sm_mhz") or (clocks or {}).get("sm_max_mhz")
+    if not mhz:
+        return None
+    achieved = tr["warp_inst_per_launch"] / (launch_ms / 1e3) / 1e9
+    peak = 148 * 4 * mhz * 1e6 / 1e9
+    return {"warp_inst_per_launch": tr["warp_inst_per_launch"], "achieved_ginst_s": achieved,
+            "peak_ginst_s": peak, "frac": achieved / peak, "sm_mhz": mhz, "capture": tr["capture"]}
 
 
 # --------------------------------------------------------------------------- reference arm
@@ -432,6 +450,7 @@ def our_arm(args, rank: int, world: int):
     dominant = ("temporal", t_ms, temporal_bytes) if t_ms >= s_ms else ("spatial", s_ms, spatial_bytes)
     achieved = dominant[2] / (dominant[1] / 1e3) / 1e9
     tr = traffic_from_profiles(dominant[0])
+    clk_now = clk.summary()
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True,
@@ -447,12 +466,13 @@ def our_arm(args, rank: int, world: int):
                      "traffic": tr["dram_bytes_per_launch"] if tr else None, "traffic_source": tr,
                      "algorithmic_bytes_per_launch": dominant[2],
                      "launch_ms": dominant[1]},
+        "issue": issue_view(tr, dominant[1], clk_now),
         "stages": {"spatial_ms": s_ms, "temporal_ms": t_ms,
                    "spatial_GBps": spatial_bytes / (s_ms / 1e3) / 1e9,
                    "temporal_GBps": temporal_bytes / (t_ms / 1e3) / 1e9,
                    "pipeline_GBps": total_bytes / (ms / 1e3) / 1e9,
                    "pipeline_frac_of_hbm": total_bytes / (ms / 1e3) / 1e9 / pk["hbm_gbs"]},
-        "clocks": clk.summary(),
+        "clocks": clk_now,
         "e2e": {"value": world * N / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(st.nbytes),
                 "d2h_bytes_per_step": int(N * plane * 8), "ms_per_step": e2e_s * 1e3,
                 "phases_s": e2e_phases, "h2d_GBps": h2d_gbps, "d2h_GBps": d2h_gbps,

@@ -98,7 +98,10 @@ def main(tag, kernels):
             rd = float(d["dram__bytes_read.sum"].replace(",", "")) * (1e9 if "G" in u["dram__bytes_read.sum"] else 1e6 if "M" in u["dram__bytes_read.sum"] else 1e3 if "K" in u["dram__bytes_read.sum"] else 1)
             wr = float(d["dram__bytes_write.sum"].replace(",", "")) * (1e9 if "G" in u["dram__bytes_write.sum"] else 1e6 if "M" in u["dram__bytes_write.sum"] else 1e3 if "K" in u["dram__bytes_write.sum"] else 1)
             stage = next(v for s, v in STAGE.items() if s in k)
-            traffic.setdefault(tag, {})[k] = {"dram_bytes": rd + wr, "stage": stage}
+            rec = {"dram_bytes": rd + wr, "stage": stage}
+            if "smsp__inst_executed.sum" in d:
+                rec["warp_inst"] = float(d["smsp__inst_executed.sum"].replace(",", ""))
+            traffic.setdefault(tag, {})[k] = rec
         except Exception:
             pass
         src = OUT / f"source_{k}_{tag}.csv"
