@@ -194,6 +194,17 @@ int ddm_b200_spatial_shard_p2p_device(const void* d_frames, int pixel_bytes, int
    d_recv is the all-to-all receive buffer, [source s][q_count][seg_frames[s]] complex;
    sequence q is the concatenation of its source segments.  Writes the lag-major map
    d_out[li * out_stride + q] (f32 or f64) for the requested lags (NULL/0 = all). */
+/* Sharded ring average, step 1 (SURVEY §8e "assembly"): per-(lag, ring) sums of one rank's
+   wave-vector slice [q_begin, q_begin + q_count) of the plane (identity layout: no cutoff in
+   the sharded run), map [n_lags][map_stride] f32 (map_f64 = 0) or f64 in HBM.  Rings are
+   llround(|q|) over the whole plane (analysis.cpp:61-97; optional q_max drops wave vectors), so
+   every rank returns the same bin_count; counts (host, bin_count) are the slice's ring
+   populations.  d_sums NULL = size query.  Step 2 (sharded.ring_average) adds the ranks' sums
+   in rank order and divides by the summed counts. */
+int ddm_b200_ring_sums_device(const void* d_map, int map_f64, int64_t q_begin, int64_t q_count,
+                              int64_t map_stride, int64_t n_lags, int width, int height, int has_q_max,
+                              double q_max, double* d_sums, int64_t capacity, int64_t* counts,
+                              int64_t* bin_count, int device, void* stream);
 int ddm_b200_temporal_segments_device(const void* d_recv, int64_t q_count, int n_segments,
                                       const int64_t* seg_frames, int precision,
                                       const int64_t* lags, int64_t n_lags, void* d_out,

@@ -216,6 +216,10 @@ void reduce_stats(const float* d, int64_t n, cudaStream_t stream, bool* finite, 
 // Deterministic ring average on device (`analysis.cpp:61-97`): values [L][plane] f64 device,
 // bins [plane] int32 (-1 = not retained), order/offsets = retained positions sorted by bin
 // (CSR), means [L][nbins] f64 device.
+// Per-(lag, ring) sums of one wave-vector slice's map [n_lags][stride] (f32 or f64, device),
+// CSR over the slice's columns in ring order: the sharded ring average.
+void ring_sums(const void* d_values, bool f64, int64_t n_lags, int64_t stride, const int64_t* d_order,
+               const int64_t* d_offsets, int64_t nbins, double* d_sums, cudaStream_t stream);
 void radial_means(const double* d_values, int64_t n_lags, int64_t plane, const int64_t* d_order,
                   const int64_t* d_offsets, int64_t nbins, double* d_means, cudaStream_t stream);
 

@@ -671,6 +671,58 @@ int ddm_b200_run_azimuthal_u16(const uint16_t* pixels, int width, int height, in
     });
 }
 
+int ddm_b200_ring_sums_device(const void* d_map, int map_f64, int64_t q_begin, int64_t q_count,
+                              int64_t map_stride, int64_t n_lags, int width, int height, int has_q_max,
+                              double q_max, double* d_sums, int64_t capacity, int64_t* counts,
+                              int64_t* bin_count, int device, void* stream) {
+    return guarded([&] {
+        if (width < 1 || height < 1 || n_lags < 0 || q_begin < 0 || q_count < 0)
+            throw ddm::InputError("ring sums: bad geometry");
+        const int Wh = ddm::half_cols(width);
+        const int64_t plane = int64_t(height) * Wh;
+        if (q_begin + q_count > plane) throw ddm::InputError("ring sums: slice outside the plane");
+        // rings of the whole plane (`analysis.cpp:61-97`): every rank agrees on the bin count
+        auto bin_of = [&](int64_t k) {
+            return std::llround(ddm::q_magnitude(int(k / Wh), int(k % Wh), height));
+        };
+        auto kept = [&](int64_t k) {
+            return !has_q_max || ddm::q_magnitude(int(k / Wh), int(k % Wh), height) <= q_max;
+        };
+        int64_t nbins = 0;
+        for (int64_t k = 0; k < plane; ++k)
+            if (kept(k)) nbins = std::max<int64_t>(nbins, bin_of(k) + 1);
+        if (bin_count) *bin_count = nbins;
+        if (!d_sums) return;   // size query
+        if (capacity < n_lags * nbins) throw ddm::InputError("ring sums: capacity too small");
+        std::vector<int64_t> cnt(size_t(nbins), 0), off(size_t(nbins) + 1, 0), order;
+        for (int64_t j = 0; j < q_count; ++j)
+            if (kept(q_begin + j)) ++cnt[size_t(bin_of(q_begin + j))];
+        for (int64_t b = 0; b < nbins; ++b) off[size_t(b) + 1] = off[size_t(b)] + cnt[size_t(b)];
+        order.resize(size_t(off.back()));
+        std::vector<int64_t> fill(off.begin(), off.end() - 1);
+        for (int64_t j = 0; j < q_count; ++j)
+            if (kept(q_begin + j)) order[size_t(fill[size_t(bin_of(q_begin + j))]++)] = j;
+        if (counts) std::copy(cnt.begin(), cnt.end(), counts);
+        ddm::detail::guard_device([&] {
+            auto& eng = ddm::b200::Engine::instance(device);
+            std::lock_guard<std::mutex> lock(eng.mutex());
+            on_engine_stream(eng, stream, [&] {
+                cudaStream_t st = eng.stream();
+                auto* d_idx = static_cast<int64_t*>(
+                    eng.buffer("ring_csr", (order.size() + off.size()) * sizeof(int64_t)));
+                ddm::b200::check(cudaMemcpyAsync(d_idx, order.data(), order.size() * sizeof(int64_t),
+                                                 cudaMemcpyHostToDevice, st), "upload");
+                ddm::b200::check(cudaMemcpyAsync(d_idx + order.size(), off.data(), off.size() * sizeof(int64_t),
+                                                 cudaMemcpyHostToDevice, st), "upload");
+                ddm::b200::ring_sums(d_map, map_f64 != 0, n_lags, map_stride, d_idx, d_idx + order.size(),
+                                     nbins, d_sums, st);
+                ddm::b200::check(cudaStreamSynchronize(st), "sync");   // host CSR vectors
+            });
+            return 0;
+        });
+    });
+}
+
 int ddm_b200_fit_rings(const double* means, const int64_t* lags, int64_t n_lags,
                        const int64_t* counts, int64_t nbins, double frame_interval, int device,
                        double* amplitude, double* baseline, double* tau, double* residual,

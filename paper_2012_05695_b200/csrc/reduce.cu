@@ -62,6 +62,22 @@ __global__ void radial_kernel(const double* __restrict__ values, int64_t n_lags,
     if (lane == 0) means[wid] = hi > lo ? acc / (double)(hi - lo) : 0.0;
 }
 
+// one warp per (lag, bin): the bin's sum over this slice's columns order[off[b] .. off[b+1])
+template <typename T>
+__global__ void ring_sums_kernel(const T* __restrict__ values, int64_t n_lags, int64_t stride,
+                                 const int64_t* __restrict__ order, const int64_t* __restrict__ off,
+                                 int64_t nbins, double* __restrict__ sums) {
+    const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (wid >= n_lags * nbins) return;
+    const int64_t li = wid / nbins, b = wid - li * nbins;
+    const T* row = values + li * stride;
+    double acc = 0.0;
+    for (int64_t j = off[b] + lane; j < off[b + 1]; j += 32) acc += (double)row[order[j]];
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) sums[wid] = acc;
+}
+
 }  // namespace
 
 template <typename T>
@@ -95,6 +111,21 @@ void reduce_stats(const double* d, int64_t n, cudaStream_t stream, bool* finite,
 void reduce_stats(const float* d, int64_t n, cudaStream_t stream, bool* finite, double* max_v,
                   double* min_v) {
     reduce_stats_t(d, n, stream, finite, max_v, min_v);
+}
+
+void ring_sums(const void* d_values, bool f64, int64_t n_lags, int64_t stride, const int64_t* d_order,
+               const int64_t* d_offsets, int64_t nbins, double* d_sums, cudaStream_t stream) {
+    const int64_t warps = n_lags * nbins;
+    const int threads = 256;
+    const int64_t blocks = (warps * 32 + threads - 1) / threads;
+    if (blocks == 0) return;
+    if (f64)
+        ring_sums_kernel<double><<<(unsigned)blocks, threads, 0, stream>>>(
+            static_cast<const double*>(d_values), n_lags, stride, d_order, d_offsets, nbins, d_sums);
+    else
+        ring_sums_kernel<float><<<(unsigned)blocks, threads, 0, stream>>>(
+            static_cast<const float*>(d_values), n_lags, stride, d_order, d_offsets, nbins, d_sums);
+    check(cudaGetLastError(), "ring sums kernel");
 }
 
 void radial_means(const double* d_values, int64_t n_lags, int64_t plane, const int64_t* d_order,

@@ -120,6 +120,62 @@ class DeviceOps:
         self.temporal_ms = ms.value
 
 
+    def ring_sums(self, out, q_begin: int, q_count: int, out_stride: int, n_lags: int,
+                  out_f64: bool = False, q_max: Optional[float] = None):
+        """Per-(lag, ring) sums of this rank's slice [q_begin, q_begin + q_count) of the map
+        (device tensor [n_lags][out_stride]) -> (sums: device f64 tensor [n_lags, bins],
+        counts: numpy int64 [bins]). Every rank gets the same bin count."""
+        import torch
+        nb = C.c_int64(0)
+        args = (C.c_int64(q_begin), C.c_int64(q_count), C.c_int64(out_stride), C.c_int64(n_lags),
+                self.width, self.height, 0 if q_max is None else 1, C.c_double(q_max or 0.0))
+        ddm._check(ddm.lib().ddm_b200_ring_sums_device(
+            C.c_void_p(out.data_ptr()), 1 if out_f64 else 0, *args, None, C.c_int64(0), None,
+            C.byref(nb), self.device, C.c_void_p(self._stream())))
+        sums = torch.empty(n_lags, nb.value, dtype=torch.float64, device=out.device)
+        counts = np.zeros(max(nb.value, 1), dtype=np.int64)
+        ddm._check(ddm.lib().ddm_b200_ring_sums_device(
+            C.c_void_p(out.data_ptr()), 1 if out_f64 else 0, *args, C.c_void_p(sums.data_ptr()),
+            C.c_int64(sums.numel()), ddm._p(counts, C.c_int64), C.byref(nb), self.device,
+            C.c_void_p(self._stream())))
+        return sums, counts[: nb.value]
+
+
+def combine_ring_sums(sums: Sequence, counts: Sequence):
+    """Ring means from the ranks' (sums, counts), added in rank order (deterministic):
+    mean = sum / count, empty rings 0 (`analysis.cpp:61-97`). Works on torch tensors or numpy."""
+    total = sums[0].clone() if hasattr(sums[0], "clone") else np.array(sums[0], dtype=np.float64)
+    for t in sums[1:]:
+        total += t
+    cnt = np.asarray(counts[0], dtype=np.int64).copy()
+    for c in counts[1:]:
+        cnt += np.asarray(c, dtype=np.int64)
+    if hasattr(total, "clone"):
+        import torch
+        ct = torch.as_tensor(cnt, device=total.device)
+        means = torch.where(ct > 0, total / ct.clamp(min=1).to(total.dtype), torch.zeros_like(total))
+    else:
+        means = np.where(cnt > 0, total / np.maximum(cnt, 1), 0.0)
+    return means, cnt
+
+
+def ring_average(sums, counts, group=None):
+    """Sharded ring average, step 2: gather every rank's [lags, bins] sums and
+    ring counts (a few MB), add them in rank order and divide. Returns (means, counts) on
+    every rank."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return combine_ring_sums([sums], [counts])
+    world = dist.get_world_size(group)
+    ct = torch.as_tensor(np.asarray(counts, dtype=np.int64), device=sums.device)
+    s_all = [torch.empty_like(sums) for _ in range(world)]
+    c_all = [torch.empty_like(ct) for _ in range(world)]
+    dist.all_gather(s_all, sums.contiguous(), group=group)
+    dist.all_gather(c_all, ct, group=group)
+    return combine_ring_sums(s_all, [c.cpu().numpy() for c in c_all])
+
+
 class ShardedRun:
     """One rank of a sharded WITH_FT run. Buffers are allocated once and reused per step.
 

@@ -248,3 +248,82 @@ def test_gpu_virtual_ranks_vs_oracle(W, H, N, G, precision, lags):
     tol = 1e-4 if precision == "f32" else 1e-10
     assert O.relative_l2(got, ref) <= tol
 
+
+
+# --------------------------------------------------------------------------- sharded ring average
+
+def _ring_worker(rank, world, port, result_path):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # rank r's slice of a 20 x 17 plane map (3 lags): its ring sums and counts, by the
+        # oracle's ring assignment; ring_average must equal the whole-map ring means
+        W, H, L = 32, 20, 3
+        Q = H * (W // 2 + 1)
+        vals = np.random.default_rng(3).uniform(0, 5, size=(L, Q))
+        plan = sharded.plan_shards(Q, 8 * world, world)
+        b, e = plan.q_begin[rank], plan.q_begin[rank + 1]
+        hc = W // 2 + 1
+        ks = np.arange(Q)
+        bins = np.floor(O.q_magnitude(ks // hc, ks % hc, H) + 0.5).astype(np.int64)
+        nb = int(bins.max()) + 1
+        sums = np.zeros((L, nb))
+        for li in range(L):
+            sums[li] = np.bincount(bins[b:e], weights=vals[li, b:e], minlength=nb)
+        counts = np.bincount(bins[b:e], minlength=nb)
+        means, cnt = sharded.ring_average(torch.from_numpy(sums), counts)
+        if rank == 0:
+            np.save(result_path, {"means": means.numpy(), "counts": cnt, "vals": vals}, allow_pickle=True)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_ring_average_matches_whole_map(tmp_path, world):
+    import torch.multiprocessing as mp
+    out = tmp_path / "ring.npy"
+    mp.spawn(_ring_worker, args=(world, _free_port(), str(out)), nprocs=world, join=True)
+    r = np.load(out, allow_pickle=True).item()
+    means, counts = O.azimuthal_average(r["vals"].reshape(3, 20, 17), 32, 20)
+    assert np.array_equal(r["counts"], counts)
+    assert np.allclose(r["means"], means, rtol=1e-12, atol=0)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("G", [1, 2, 3])
+def test_gpu_sharded_ring_sums_match_azimuthal(G):
+    """Per-rank ring sums (ddm_b200_ring_sums_device) over the sharded temporal outputs,
+    added in rank order, equal the ring means of the assembled map (`analysis.cpp:61-97`)."""
+    import torch
+    from paper_2012_05695_b200 import ddm
+    W, H, N = 64, 48, 96
+    st = ddm.generate(W, H, N, particles=30, seed=12)
+    Q = H * (W // 2 + 1)
+    plan = sharded.plan_shards(Q, N, G)
+    ops = sharded.DeviceOps(W, H, "f32", device=0)
+    frames = torch.from_numpy(st.view(np.int16)).cuda()
+    sends = []
+    for r in range(G):
+        send = torch.empty(2 * Q * plan.frames_of(r), dtype=torch.float32, device="cuda")
+        ops.spatial(frames[plan.frame_begin[r]: plan.frame_begin[r + 1]], plan.frames_of(r), send)
+        sends.append(send)
+    sums, counts, parts = [], [], []
+    for d in range(G):
+        chunks = [sends[s][2 * plan.q_begin[d] * plan.frames_of(s): 2 * plan.q_begin[d + 1] * plan.frames_of(s)]
+                  for s in range(G)]
+        q_d = plan.q_of(d)
+        out = torch.empty(N * q_d, dtype=torch.float32, device="cuda")
+        ops.temporal(torch.cat(chunks), q_d, [plan.frames_of(s) for s in range(G)], out, q_d)
+        s_d, c_d = ops.ring_sums(out, plan.q_begin[d], q_d, q_d, N)
+        sums.append(s_d)
+        counts.append(c_d)
+        parts.append(out.view(N, q_d).cpu().numpy().astype(np.float64))
+    means, cnt = sharded.combine_ring_sums(sums, counts)
+    full = sharded.assemble(plan, parts)
+    ref_means, ref_counts = O.azimuthal_average(full.reshape(N, H, W // 2 + 1), W, H)
+    assert np.array_equal(cnt, ref_counts)
+    got = means.cpu().numpy()
+    assert np.abs(got - ref_means).max() <= 1e-12 * np.abs(ref_means).max()
