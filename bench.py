@@ -415,17 +415,24 @@ def our_arm(args, rank: int, world: int):
                                         C.byref(counters), C.byref(timing))
         ddm._check(rc)
 
-    for _ in range(2):
+    for _ in range(max(3, args.warmup)):
         e2e_step()
-    e2e_steps = max(3, min(args.steps, 10))
+    e2e_steps = max(5, min(args.steps, 20))
     torch.cuda.synchronize()
     phases = []
+    step_wall = []
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
+        ts = time.perf_counter()
         e2e_step()
+        step_wall.append(time.perf_counter() - ts)
         phases.append({f: float(getattr(timing, f)) for f, _ in ddm.Timing._fields_})
     torch.cuda.synchronize()
-    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    e2e_mean_s = (time.perf_counter() - t0) / e2e_steps
+    # per-call wall time: the median step. Host-side stalls of a few hundred ms hit single
+    # calls on reused boxes (measured: one 507 ms step among 32 ms ones); the mean and the
+    # per-step list are reported beside it.
+    e2e_s = statistics.median(step_wall)
     # the reference's TimingBreakdown of the C-ABI call, medians over the e2e steps (seconds):
     # disk = pinned frames H2D, step1/step2 = device kernels, merge = f64 map D2H
     e2e_phases = {f: statistics.median(p[f] for p in phases) for f in phases[0]}
@@ -476,7 +483,9 @@ def our_arm(args, rank: int, world: int):
         "e2e": {"value": world * N / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(st.nbytes),
                 "d2h_bytes_per_step": int(N * plane * 8), "ms_per_step": e2e_s * 1e3,
                 "phases_s": e2e_phases, "h2d_GBps": h2d_gbps, "d2h_GBps": d2h_gbps,
-                "path": "ddm_b200_run_u16 (C-ABI ddm::run): pinned u16 in, f64 lag-major map out"},
+                "path": "ddm_b200_run_u16 (C-ABI ddm::run): pinned u16 in, f64 lag-major map out",
+                "step_ms": [round(t * 1e3, 2) for t in step_wall],
+                "mean_ms_per_step": e2e_mean_s * 1e3, "estimator": "median over the e2e steps"},
         "gpu_launches": launches,
     }
     if world == 1 and not args.no_cpu_baseline:
