@@ -62,6 +62,9 @@ typedef struct ddm_b200_run_config {
 const char* ddm_b200_last_error(void);
 int ddm_b200_version(int* major, int* minor, int* patch);
 int ddm_b200_device_count(int* count);
+/* Diagnostics (no reference counterpart): the kernels the last run on `device` selected, e.g.
+   "spatial=rows2<256>+cols2<512> temporal=warp<1024>:map", NUL-terminated into buf. */
+int ddm_b200_last_engines(int device, char* buf, int64_t capacity);
 
 /* ddm::pad_length (proj/core/src/temporal.cpp:10-17); -1 if n < 1 */
 int64_t ddm_b200_pad_length(int64_t n);

@@ -126,6 +126,27 @@ __global__ void restore_kernel(const cpx<S>* __restrict__ seq, int64_t q, int n,
     }
 }
 
+// "spatial=... temporal=..." for last_engines()
+std::string describe(bool warp_s, int W, int H, bool warp_t, bool long_t, int64_t N2, int T,
+                     int64_t n_q, int N, bool ring) {
+    std::string s = "spatial=";
+    s += warp_s ? "rows2<" + std::to_string(W / 2) + ">+cols2<" + std::to_string(H) + ">" : "generic";
+    s += " temporal=";
+    if (warp_t) {
+        s += "warp<1024>";
+    } else if (long_t) {
+        s += "long2<" + std::to_string(N2 / 1024) + ">";
+        if (!ring) {
+            const int64_t chunk = ddmk::temporal_long_chunk(N);
+            s += " chunks=" + std::to_string((n_q + chunk - 1) / chunk);
+        }
+    } else {
+        s += "generic<T=" + std::to_string(T) + ">";
+    }
+    s += ring ? ":ring" : ":map";
+    return s;
+}
+
 template <typename S>
 void build_table(std::vector<unsigned char>& out, int len, int count) {
     out.resize((size_t)count * sizeof(cpx<S>));
@@ -257,37 +278,7 @@ void Engine::spatial_pass(ddmk::SpatialArgs sa, bool f64, bool warp_s, PhaseTime
         F = std::min(N, std::max(Fc, F - F % Fc));
     }
     last_F_ = F;
-    // register-resident path, preferred: one persistent launch schedules every row and
-    // column item of the step through a global queue (ring of nbuf L2-resident mid buffers)
-    // (opt-in: DDM_SPATIAL_FUSED=1; at 512^2 it trails the two-stream chunk pipeline below,
-    // 1.06 vs 0.92 ms, because one kernel's register budget caps the row items at 2 CTAs/SM)
-    static const char* fused_env = std::getenv("DDM_SPATIAL_FUSED");
-    const bool try_fused = warp_s && N > F && fused_env && fused_env[0] == '1';
-    if (try_fused) {
-        auto env_int = [](const char* name, int dflt) {
-            const char* e = std::getenv(name);
-            return e ? std::atoi(e) : dflt;
-        };
-        // rows run `lead` chunks ahead of the columns through a ring of nbuf = lead + 2 buffers
-        // of Ff frames (one column-CTA group each: full-length corner-turn runs), ~67 MB of L2
-        static const int lead = std::max(1, env_int("DDM_SPATIAL_LEAD", 2));
-        static const int nbuf = std::max(lead + 1, env_int("DDM_SPATIAL_NBUF", lead + 2));
-        const int Fc = ddmk::spatial_warp_col_frames(sa.H);
-        int Ff = std::max(Fc, env_int("DDM_SPATIAL_F", Fc));
-        Ff = std::min(N, Ff - Ff % Fc);
-        const int K = (N + Ff - 1) / Ff;
-        last_F_ = Ff;
-        sa.mid = mid_.ensure((size_t)Ff * per_frame * nbuf);
-        int* sync = static_cast<int*>(buffer("spatial_sync", (size_t)(1 + 2 * K) * sizeof(int)));
-        const cudaError_t e = ddmk::launch_spatial_fused(sa, Ff, nbuf, lead, sync, num_sms_, stream_);
-        if (e == cudaSuccess) {
-            if (times) times->spatial_launches += 1;
-            return;
-        }
-        if (e != cudaErrorNotSupported) check(e, "fused spatial kernel");
-        (void)cudaGetLastError();
-    }
-    // otherwise the row pass of chunk k+1 runs beside the column pass of chunk k on a second
+    // the row pass of chunk k+1 runs beside the column pass of chunk k on a second
     // stream, through two L2-resident `mid` buffers
     const bool overlap = warp_s && N > F && std::getenv("DDM_SPATIAL_SERIAL") == nullptr;
     void* d_mid = mid_.ensure((size_t)F * per_frame * (overlap ? 2 : 1));
@@ -409,6 +400,7 @@ uint64_t Engine::run(const RunSpec& sp, PhaseTimes* times) {
         evs.push_back(e);
     };
 
+    last_engines_ = describe(warp_s, W, H, warp_t, long_t, N2, T, gmax, N, false);
     uint64_t spatial_passes = 0;
     for (size_t gi = 0; gi < sp.groups.size(); ++gi) {
         const int64_t gb = sp.groups[gi].first, gc = sp.groups[gi].second - gb;
@@ -667,12 +659,14 @@ bool Engine::run_rings(const RunSpec& sp, const RingPlan& rp, double* d_means, P
         if (!sp.identity)
             check(cudaMemsetAsync(m.d_out, 0, (size_t)(L * m.out_stride) * sizeof(double), stream_), "memset");
         run(m, times);
+        last_engines_ += "+radial";
         radial_means(static_cast<const double*>(m.d_out), L, m.out_stride, rc.flat_by_bin, rc.bin_off,
                      rp.nbins, d_means, stream_);
         check(cudaStreamSynchronize(stream_), "sync");
         return false;
     }
     // fused: spatial pass into the slot-major spectra, then the ring temporal launch
+    last_engines_ = describe(warp_s, sp.W, sp.H, warp_t, long_t, N2, 1, count, N, true);
     const int* d_lag_index = upload_lags(sp.lags, N);
     const int Wh = sp.W / 2 + 1;
     const int64_t plane = (int64_t)sp.H * Wh;

@@ -152,6 +152,10 @@ public:
 
     // Last spatial-chunk / tile geometry (for reports).
     int last_tile() const { return last_T_; }
+    // Kernels the last run() / run_rings() selected, e.g.
+    // "spatial=rows2<256>+cols2<512> temporal=warp<1024>:map" (tests assert on it, so a shape
+    // cannot silently fall back to the generic engines)
+    const std::string& last_engines() const { return last_engines_; }
     int last_chunk_frames() const { return last_F_; }
 
     std::mutex& mutex() { return mu_; }
@@ -178,6 +182,7 @@ private:
     std::map<std::pair<int, int>, std::unique_ptr<DeviceBuffer>> post_;
     std::map<std::string, std::unique_ptr<DeviceBuffer>> named_;
     int last_T_ = 0, last_F_ = 0;
+    std::string last_engines_;
     std::vector<int> lag_cache_;               // lag slots last uploaded to lagidx_
     std::vector<cudaEvent_t> timing_events_;   // reusable phase-timing events
     std::vector<cudaEvent_t> chunk_events_;    // row/column pass ordering across streams

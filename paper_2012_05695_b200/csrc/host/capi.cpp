@@ -141,6 +141,18 @@ int ddm_b200_device_count(int* count) {
     });
 }
 
+int ddm_b200_last_engines(int device, char* buf, int64_t capacity) {
+    return guarded([&] {
+        if (!buf || capacity < 1) throw ddm::InputError("null or empty buffer");
+        auto& eng = ddm::b200::Engine::instance(device);
+        std::lock_guard<std::mutex> lock(eng.mutex());
+        const std::string& s = eng.last_engines();
+        const size_t n = std::min<size_t>(s.size(), (size_t)capacity - 1);
+        std::memcpy(buf, s.data(), n);
+        buf[n] = '\0';
+    });
+}
+
 int64_t ddm_b200_pad_length(int64_t n) {
     if (n < 1) return -1;
     return ddm::pad_length(n);

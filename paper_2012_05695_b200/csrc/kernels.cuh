@@ -145,11 +145,7 @@ cudaError_t launch_temporal_long(const TemporalArgs& a, int num_sms, void* out_q
 // Register-resident spatial kernels (spatial_warp.cu): f32, power-of-two W/2 and H in
 // [16, 1024], u16/u8 frames, wave-vector-major output (layout T = 1).
 bool spatial_warp_supported(int W, int H, int pixel_bytes, int scalar_bytes);
-// The whole spatial step in one persistent launch (row and column items scheduled through
-// a global queue, `nbuf` L2-resident mid buffers of F frames, `sync` = 1 + 2 ceil(N/F)
-// ints). Square-ish power-of-two frames (512^2, 1024^2, 256^2); cudaErrorNotSupported else.
-cudaError_t launch_spatial_fused(const SpatialArgs& a, int F, int nbuf, int lead, int* sync,
-                                 int num_sms, cudaStream_t stream);
+
 // frames one column-pass CTA transforms together (the run length of its corner-turn stores)
 int spatial_warp_col_frames(int H);
 // parts: 1 = row pass (frames -> mid), 2 = column pass (mid -> spectra), 3 = both

@@ -130,8 +130,6 @@ __device__ __forceinline__ void st_stream(cpx<S>* p, cpx<S> v) {
 }
 
 // ---------------------------------------------------------------------------- cols
-// kCoherent: `mid` was written by other CTAs of the same launch (the fused spatial kernel),
-// so it is read through L2 (ld.global.cg), never a stale L1 line.
 // Column-pass epilogue: the CTA's transposed stage sm[r * (F + 1) + f] (wave-vector row r,
 // frame f of this CTA's nf frames starting at n0, column c) -> the spectra, a peer's receive
 // buffer, or a cutoff / group subset.
@@ -191,7 +189,7 @@ __device__ __forceinline__ void cols_epilogue(const cpx<S>* sm, int Wh, int N, i
     }
 }
 
-template <typename S, int HL, bool kCoherent>
+template <typename S, int HL>
 __device__ __forceinline__ void cols2_body(const cpx<S>* __restrict__ mid, int Wh, int N, int frame0,
                                            int nframes, const cpx<S>* __restrict__ tw_col,
                                            cpx<S>* __restrict__ spec, const SpecLayout& lay,
@@ -216,17 +214,8 @@ __device__ __forceinline__ void cols2_body(const cpx<S>* __restrict__ mid, int W
     cpx<S> v[B];
     if (g < nf) {
         const cpx<S>* col = mid + ((size_t)(f0 + g) * Wh + c) * HL;
-        if constexpr (kCoherent && sizeof(S) == 4) {
-            const float2* c2 = reinterpret_cast<const float2*>(col);
 #pragma unroll
-            for (int b = 0; b < B; ++b) {
-                const float2 t = __ldcs(c2 + a + A * b);      // L2, last use
-                v[b] = {t.x, t.y};
-            }
-        } else {
-#pragma unroll
-            for (int b = 0; b < B; ++b) v[b] = col[a + A * b];
-        }
+        for (int b = 0; b < B; ++b) v[b] = col[a + A * b];
         group_fft<A, B, -1, S>(v, sm + g * REG, a, tw);
         {
             // the row-pass buffer has been consumed: drop its L2 lines without writing
@@ -254,7 +243,7 @@ cols2_kernel(const cpx<S>* __restrict__ mid, int Wh, int N, int frame0, int nfra
              const cpx<S>* __restrict__ tw_col, cpx<S>* __restrict__ spec, SpecLayout lay,
              const int* __restrict__ slot_of_flat, const __grid_constant__ PeerTable peers) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    cols2_body<S, HL, false>(mid, Wh, N, frame0, nframes, tw_col, spec, lay, slot_of_flat, peers,
+    cols2_body<S, HL>(mid, Wh, N, frame0, nframes, tw_col, spec, lay, slot_of_flat, peers,
                              blockIdx.x, smem_raw);
 }
 
@@ -281,23 +270,26 @@ constexpr size_t cols_smem(size_t cs) {
 }
 
 template <typename S, typename Pix, int L>
-void launch_rows2(const SpatialArgs& a, cudaStream_t st) {
+cudaError_t launch_rows2(const SpatialArgs& a, cudaStream_t st) {
     auto k = rows2_kernel<S, Pix, L>;
     const size_t smem = rows_smem<L>(sizeof(cpx<S>));
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
     constexpr int RB = kThreads / split_a<L>();
     const int grid = a.nframes * ((a.H + RB - 1) / RB);
     k<<<grid, kThreads, smem, st>>>(static_cast<const Pix*>(a.frames), a.H, a.frame0,
                                     static_cast<const cpx<S>*>(a.tw_row.ptr),
                                     static_cast<const cpx<S>*>(a.tw_post.ptr),
                                     static_cast<cpx<S>*>(a.mid));
+    return cudaGetLastError();
 }
 
 template <typename S, int HL>
-void launch_cols2(const SpatialArgs& a, cudaStream_t st) {
+cudaError_t launch_cols2(const SpatialArgs& a, cudaStream_t st) {
     auto k = cols2_kernel<S, HL>;
     const size_t smem = cols_smem<HL>(sizeof(cpx<S>));
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
     constexpr int F = kThreads / split_a<HL>();
     const int Wh = a.W / 2 + 1;
     const int grid = Wh * ((a.nframes + F - 1) / F);
@@ -305,129 +297,6 @@ void launch_cols2(const SpatialArgs& a, cudaStream_t st) {
                                     a.nframes, static_cast<const cpx<S>*>(a.tw_col.ptr),
                                     static_cast<cpx<S>*>(a.spec), a.layout,
                                     a.slot_of_flat, a.peers);
-}
-
-// ---------------------------------------------------------------------------- fused
-// One persistent launch for the whole spatial step: CTAs take work items from a global
-// counter in the order R0 | R1 C0 | R2 C1 | ... | C(K-1), where R(k) are the row-pass items
-// of frame chunk k and C(k) its column-pass items. Chunk k's `mid` is ring buffer k % NB.
-// C(k) waits until every R(k) item is done; R(k) waits until C(k - NB) has released its
-// buffer. Every dependency points to items dequeued earlier, so the queue always drains;
-// there are no launch gaps or per-chunk tails, and row and column work overlap freely.
-struct FusedSched {
-    int K, F, N, nbuf, lead, rblocks, Wh, Fc;
-    size_t buf_elems;               // complex values per mid buffer
-    int* sync;                      // [0] work counter, [1..K] rows done, [K+1..2K] cols done
-    __device__ int nf(int k) const { return min(F, N - k * F); }
-    __device__ int n_rows(int k) const { return nf(k) * rblocks; }
-    __device__ int n_cols(int k) const { return Wh * ((nf(k) + Fc - 1) / Fc); }
-    // segment s -> (is_cols, chunk): R(0..D-1), then pairs (R(j + D), C(j)), then the last
-    // D column segments; D = lead (rows run D chunks ahead of the columns)
-    __device__ void seg(int s, bool& cols, int& k) const {
-        const int D = min(lead, K), P = K - D;
-        if (s < D) { cols = false; k = s; return; }
-        const int t = s - D;
-        if (t < 2 * P) { cols = (t & 1); k = (t & 1) ? t / 2 : t / 2 + D; return; }
-        cols = true;
-        k = P + (t - 2 * P);
-    }
-    __device__ int seg_size(int s) const {
-        bool c; int k;
-        seg(s, c, k);
-        return c ? n_cols(k) : n_rows(k);
-    }
-    __device__ int total() const {
-        int t = 0;
-        for (int k = 0; k < K; ++k) t += n_rows(k) + n_cols(k);
-        return t;
-    }
-};
-
-__device__ __forceinline__ void wait_count(const int* p, int target) {
-    while (atomicAdd(const_cast<int*>(p), 0) < target) __nanosleep(64);
-    __threadfence();
-}
-
-template <typename S, typename Pix, int L, int HL>
-__global__ void __launch_bounds__(kThreads, 2)
-spatial_fused_kernel(const Pix* __restrict__ frames, int H, const cpx<S>* __restrict__ tw_row,
-                     const cpx<S>* __restrict__ tw_post, const cpx<S>* __restrict__ tw_col,
-                     cpx<S>* __restrict__ mid, cpx<S>* __restrict__ spec, SpecLayout lay,
-                     const int* __restrict__ slot_of_flat, const __grid_constant__ PeerTable peers,
-                     const FusedSched sc) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ int s_item, s_cols, s_chunk, s_idx;
-    const int total = sc.total();
-    int seg = 0, seg_start = 0;     // thread 0's cursor (items only increase)
-    // thread 0 claims the following item while the current one is processed, so the atomic's
-    // round trip never stalls the CTA (the smallest unfinished item is always running or
-    // queued behind a smaller one: the queue still drains)
-    int next = threadIdx.x == 0 ? atomicAdd(sc.sync, 1) : 0;
-    for (;;) {
-        if (threadIdx.x == 0) {
-            const int item = next;
-            if (item < total) next = atomicAdd(sc.sync, 1);
-            s_item = item;
-            if (item < total) {
-                while (item >= seg_start + sc.seg_size(seg)) {
-                    seg_start += sc.seg_size(seg);
-                    ++seg;
-                }
-                bool c; int k;
-                sc.seg(seg, c, k);
-                s_cols = c;
-                s_chunk = k;
-                s_idx = item - seg_start;
-                if (c) wait_count(sc.sync + 1 + k, sc.n_rows(k));
-                else if (k >= sc.nbuf) wait_count(sc.sync + 1 + sc.K + (k - sc.nbuf), sc.n_cols(k - sc.nbuf));
-            }
-        }
-        __syncthreads();
-        if (s_item >= total) break;
-        const int k = s_chunk, idx = s_idx;
-        cpx<S>* buf = mid + (size_t)(k % sc.nbuf) * sc.buf_elems;
-        if (s_cols) {
-            cols2_body<S, HL, true>(buf, sc.Wh, sc.N, k * sc.F, sc.nf(k), tw_col, spec, lay,
-                                    slot_of_flat, peers, idx, smem_raw);
-        } else {
-            rows2_body<S, Pix, L>(frames, H, k * sc.F, tw_row, tw_post, buf, idx, smem_raw);
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            __threadfence();
-            atomicAdd(sc.sync + 1 + (s_cols ? sc.K : 0) + k, 1);
-        }
-    }
-}
-
-template <typename S, typename Pix, int L, int HL>
-cudaError_t launch_fused_t(const SpatialArgs& a, int F, int nbuf, int lead, int* sync, int num_sms,
-                           cudaStream_t st) {
-    auto k = spatial_fused_kernel<S, Pix, L, HL>;
-    const size_t smem = std::max(rows_smem<L>(sizeof(cpx<S>)), cols_smem<HL>(sizeof(cpx<S>)));
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    int occ = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kThreads, smem);
-    if (e != cudaSuccess) return e;
-    FusedSched sc;
-    sc.N = a.N;
-    sc.F = F;
-    sc.K = (a.N + F - 1) / F;
-    sc.nbuf = nbuf;
-    sc.lead = lead;
-    sc.rblocks = a.H / (kThreads / split_a<L>());
-    sc.Wh = a.W / 2 + 1;
-    sc.Fc = kThreads / split_a<HL>();
-    sc.buf_elems = (size_t)F * sc.Wh * a.H;
-    sc.sync = sync;
-    e = cudaMemsetAsync(sync, 0, (size_t)(1 + 2 * sc.K) * sizeof(int), st);
-    if (e != cudaSuccess) return e;
-    k<<<std::max(1, occ) * num_sms, kThreads, smem, st>>>(
-        static_cast<const Pix*>(a.frames), a.H, static_cast<const cpx<S>*>(a.tw_row.ptr),
-        static_cast<const cpx<S>*>(a.tw_post.ptr), static_cast<const cpx<S>*>(a.tw_col.ptr),
-        static_cast<cpx<S>*>(a.mid), static_cast<cpx<S>*>(a.spec), a.layout, a.slot_of_flat,
-        a.peers, sc);
     return cudaGetLastError();
 }
 
@@ -451,47 +320,32 @@ int spatial_warp_col_frames(int H) {
 template <typename S>
 cudaError_t launch_spatial_warp(const SpatialArgs& a, cudaStream_t stream, int parts) {
     const int L = a.W / 2;
+    cudaError_t e = cudaSuccess;
     if (parts & 1) {
 #define DDMK_R2(LEN)                                                               \
     case LEN:                                                                      \
-        if (a.pixel_bytes == 2) launch_rows2<S, uint16_t, LEN>(a, stream);         \
-        else launch_rows2<S, uint8_t, LEN>(a, stream);                             \
+        e = a.pixel_bytes == 2 ? launch_rows2<S, uint16_t, LEN>(a, stream)          \
+                               : launch_rows2<S, uint8_t, LEN>(a, stream);          \
         break;
     switch (L) {
         DDMK_R2(16) DDMK_R2(32) DDMK_R2(64) DDMK_R2(128) DDMK_R2(256) DDMK_R2(512) DDMK_R2(1024)
     default: return cudaErrorInvalidValue;
     }
 #undef DDMK_R2
-    cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     }
     if (!(parts & 2)) return cudaSuccess;
 #define DDMK_C2(LEN) \
-    case LEN: launch_cols2<S, LEN>(a, stream); break;
+    case LEN: e = launch_cols2<S, LEN>(a, stream); break;
     switch (a.H) {
         DDMK_C2(16) DDMK_C2(32) DDMK_C2(64) DDMK_C2(128) DDMK_C2(256) DDMK_C2(512) DDMK_C2(1024)
         DDMK_C2(2048)
     default: return cudaErrorInvalidValue;
     }
 #undef DDMK_C2
-    return cudaGetLastError();
+    return e;
 }
 
 template cudaError_t launch_spatial_warp<float>(const SpatialArgs&, cudaStream_t, int);
-
-cudaError_t launch_spatial_fused(const SpatialArgs& a, int F, int nbuf, int lead, int* sync,
-                                 int num_sms, cudaStream_t stream) {
-    // R(k) waits for C(k - nbuf), which the queue must hold earlier: nbuf > lead >= 1
-    if (lead < 1 || nbuf <= lead) return cudaErrorInvalidValue;
-    const int L = a.W / 2;
-#define DDMK_F(LEN, HLEN)                                                                   \
-    if (L == LEN && a.H == HLEN)                                                            \
-        return a.pixel_bytes == 2                                                           \
-                   ? launch_fused_t<float, uint16_t, LEN, HLEN>(a, F, nbuf, lead, sync, num_sms, stream) \
-                   : launch_fused_t<float, uint8_t, LEN, HLEN>(a, F, nbuf, lead, sync, num_sms, stream);
-    DDMK_F(256, 512) DDMK_F(512, 1024) DDMK_F(128, 256)
-#undef DDMK_F
-    return cudaErrorNotSupported;
-}
 
 }  // namespace ddmk

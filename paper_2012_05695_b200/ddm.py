@@ -102,6 +102,13 @@ def device_count() -> int:
     return n.value
 
 
+def last_engines(device: int = 0) -> str:
+    """The kernels the last run on `device` selected ("spatial=... temporal=...")."""
+    buf = C.create_string_buffer(256)
+    _check(lib().ddm_b200_last_engines(device, buf, C.c_int64(256)))
+    return buf.value.decode()
+
+
 def pad_length(n: int) -> int:
     v = lib().ddm_b200_pad_length(n)
     if v < 0:

@@ -402,10 +402,13 @@ def test_long_sequences_ring_average(ddm, W, H, N):
 
 @pytest.mark.gpu
 def test_tall_frames_column_pass(ddm):
-    """H = 2048 register column pass (the 2048^2 geometry), small width and frame count."""
-    st = O.random_stack(32, 2048, 40, seed=21)
-    got = ddm.run(st, ddm.RunConfig(precision="f32", memory_bytes=1 << 40)).values
-    assert O.relative_l2(got, O.run_with_ft(st, "f32")) <= 1e-4
+    """H = 2048 register column pass (cols2<2048>, the 2048^2 geometry) with the warp temporal
+    engine (N = 600 > 512), small width; wave-vector subset against the oracle."""
+    st = O.random_stack(32, 2048, 600, seed=21)
+    got, ref = _subset_check(ddm, st, "f32", n_q=2048, seed=21)
+    eng = ddm.last_engines()
+    assert "cols2<2048>" in eng and "warp<1024>" in eng, eng
+    assert O.relative_l2(got, ref) <= 1e-4
     sp = ddm.compute_spectra(st[:3], "f32")
     ref = O.spectra(st[:3], "f64")
     assert np.linalg.norm((sp - ref).ravel()) <= 1e-5 * np.linalg.norm(ref.ravel())
