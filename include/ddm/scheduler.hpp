@@ -57,6 +57,7 @@ struct LagChunk {
 struct ChunkPlan {
     std::int64_t capacity = 0;
     std::vector<LagChunk> chunks;
+    std::int64_t passes() const { return std::int64_t(chunks.size()); }
 };
 ChunkPlan plan_without_ft(std::int64_t frames, std::vector<std::int64_t> lags,
                           const MemoryBudget& budget, std::int64_t bytes_per_spectrum);

@@ -328,6 +328,9 @@ const int* Engine::upload_lags(const std::vector<int64_t>& lags, int N) {
     std::vector<int> lag_index((size_t)N, -1);
     for (size_t li = 0; li < lags.size(); ++li) lag_index[(size_t)lags[li]] = (int)li;
     if (lag_index != lag_cache_) {
+        // kernels already queued on stream_ (asynchronous device-resident calls) may still
+        // read the previous table: drain them before it is overwritten
+        check(cudaStreamSynchronize(stream_), "sync before lag upload");
         check(cudaMemcpy(lagidx_.ensure((size_t)N * sizeof(int)), lag_index.data(),
                          (size_t)N * sizeof(int), cudaMemcpyHostToDevice), "lag upload");
         lag_cache_ = std::move(lag_index);

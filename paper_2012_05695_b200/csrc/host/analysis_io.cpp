@@ -23,7 +23,10 @@ std::string to_string(ExponentialFit::Flag flag) {
     return "?";
 }
 
-std::vector<ExponentialFit> fit_all_bins(const RadialProfile& p) {
+namespace {
+
+// fit_all_bins on a chosen device (analyze passes RunConfig::device)
+std::vector<ExponentialFit> fit_all_bins_on(const RadialProfile& p, int device) {
     std::vector<ExponentialFit> fits;
     std::int64_t usable = 0;
     for (const auto m : p.lags)
@@ -33,7 +36,7 @@ std::vector<ExponentialFit> fit_all_bins(const RadialProfile& p) {
     std::vector<double> out(4 * B);
     std::vector<int> flag(B);
     detail::guard_device([&] {
-        b200::Engine& eng = b200::Engine::instance(0);
+        b200::Engine& eng = b200::Engine::instance(device);
         std::lock_guard<std::mutex> lock(eng.mutex());
         cudaStream_t st = eng.stream();
         char* base = static_cast<char*>(eng.buffer("fit_io", L * B * 8 + L * 8 + B * 8 + 4 * B * 8 + B * 4));
@@ -67,6 +70,10 @@ std::vector<ExponentialFit> fit_all_bins(const RadialProfile& p) {
     }
     return fits;
 }
+
+}  // namespace
+
+std::vector<ExponentialFit> fit_all_bins(const RadialProfile& p) { return fit_all_bins_on(p, 0); }
 
 DiffusionEstimate estimate_diffusion(const std::vector<ExponentialFit>& fits, std::int64_t width,
                                      std::int64_t q_lo, std::int64_t q_hi) {
@@ -143,7 +150,7 @@ ResultArchive analyze(FrameSource& source, RunConfig config, const fs::path& out
     const RadialProfile profile = azimuthal_average(a.map, wv);
     trace.lap("azimuthal");
     write_radial_csv(profile, out_dir / "radial.csv");
-    const auto fits = fit_all_bins(profile);
+    const auto fits = fit_all_bins_on(profile, config.device);
     if (!fits.empty()) write_fits_csv(fits, out_dir / "fits.csv");
     trace.lap("fits+csv");
     return a;
@@ -153,7 +160,7 @@ ResultArchive analyze(FrameSource& source, RunConfig config, const fs::path& out
 
 namespace ddm {
 
-double relative_deviation(const ResultMap& a, const ResultMap& b) {
+double b200::relative_deviation(const ResultMap& a, const ResultMap& b) {
     double peak = 0.0;
     for (const double v : a.values) peak = std::max(peak, std::abs(v));
     for (const double v : b.values) peak = std::max(peak, std::abs(v));
@@ -171,7 +178,7 @@ CompareReport compare(FrameSource& source, const RunConfig& config, Algorithm a,
         r.algorithms[i] = out[i].algorithm;
         r.timing[i] = out[i].timing;
     }
-    r.deviation = relative_deviation(out[0].map, out[1].map);
+    r.deviation = b200::relative_deviation(out[0].map, out[1].map);
     r.tolerance = config.precision == Precision::F32 ? 1e-4 : 1e-9;
     r.pass = r.deviation <= r.tolerance;
     return r;

@@ -87,6 +87,12 @@ LagProfile SequenceEngine<Scalar>::with_ft(std::span<const std::complex<Scalar>>
 }
 
 template <typename Scalar>
+std::vector<double> SequenceEngine<Scalar>::correlation(std::span<const std::complex<Scalar>> seq) {
+    // the engine's corr is restored to the original basis: the raw sum of `temporal.cpp:48-75`
+    return with_ft(seq).corr;
+}
+
+template <typename Scalar>
 std::vector<double> SequenceEngine<Scalar>::with_ft_batch(std::span<const std::complex<Scalar>> seqs) {
     if (seqs.size() % std::size_t(frames_) != 0)
         throw InputError("SequenceEngine: batch is not a whole number of sequences");
@@ -113,6 +119,47 @@ LagProfile with_ft_sequence(std::span<const std::complex<Scalar>> seq, RunCounte
     return p;
 }
 
+template <typename Scalar>
+std::vector<double> averages_term(std::span<const std::complex<Scalar>> seq) {
+    SequenceEngine<Scalar> engine(std::int64_t(seq.size()));
+    return engine.with_ft(seq).d_a;
+}
+
+template <typename Scalar>
+std::vector<double> correlation_term(std::span<const std::complex<Scalar>> seq, RunCounters* counters) {
+    SequenceEngine<Scalar> engine(std::int64_t(seq.size()));
+    std::vector<double> c = engine.correlation(seq);
+    if (counters) counters->temporal_ffts += engine.temporal_fft_count();
+    return c;
+}
+
+LagProfile direct_sequence_oracle(std::span<const std::complex<double>> seq) {
+    const auto n = std::int64_t(seq.size());
+    if (n < 1) throw InputError("direct_sequence_oracle: empty sequence");
+    LagProfile out;
+    out.d.resize(seq.size());
+    out.d_a.resize(seq.size());
+    out.corr.resize(seq.size());
+    for (std::int64_t m = 0; m < n; ++m) {
+        double sd = 0.0, sa = 0.0, sc = 0.0;
+        for (std::int64_t k = m; k < n; ++k) {
+            const auto a = seq[std::size_t(k - m)], b = seq[std::size_t(k)];
+            sd += std::norm(a - b);
+            sa += std::norm(a) + std::norm(b);
+            sc += a.real() * b.real() + a.imag() * b.imag();
+        }
+        const double ramp = double(n - m);
+        out.d[std::size_t(m)] = sd / ramp;
+        out.d_a[std::size_t(m)] = sa / ramp;
+        out.corr[std::size_t(m)] = sc;
+    }
+    return out;
+}
+
+template std::vector<double> averages_term<float>(std::span<const std::complex<float>>);
+template std::vector<double> averages_term<double>(std::span<const std::complex<double>>);
+template std::vector<double> correlation_term<float>(std::span<const std::complex<float>>, RunCounters*);
+template std::vector<double> correlation_term<double>(std::span<const std::complex<double>>, RunCounters*);
 template class SequenceEngine<float>;
 template class SequenceEngine<double>;
 template LagProfile with_ft_sequence<float>(std::span<const std::complex<float>>, RunCounters*);

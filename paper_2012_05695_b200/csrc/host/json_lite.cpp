@@ -138,8 +138,13 @@ void emit(const Value& v, std::string& out, int indent, int depth) {
         if (v.is_int) {
             out += std::to_string(v.i);
         } else {
+            // shortest round-trip form, as nlohmann::json prints (0.1 -> "0.1", not
+            // "0.10000000000000001")
             char buf[64];
-            std::snprintf(buf, sizeof buf, "%.17g", v.num);
+            for (int prec = 15; prec <= 17; ++prec) {
+                std::snprintf(buf, sizeof buf, "%.*g", prec, v.num);
+                if (prec == 17 || std::strtod(buf, nullptr) == v.num) break;
+            }
             std::string t = buf;
             if (t.find_first_of(".eEn") == std::string::npos) t += ".0";
             out += t;

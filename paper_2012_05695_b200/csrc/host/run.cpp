@@ -352,6 +352,9 @@ ResultArchive run_core(const Ingest& in, const RunConfig& config, double* out,
             std::memcpy(out, merged.values.data(), std::size_t(total) * sizeof(double));
             clock.stop(timing.merge);
         }
+        // the reference's run() ends with archive.validate() whatever the merge path: a
+        // before_merge hook may have edited a partial's payload
+        detail::validate_values(out, std::size_t(total), !f64);
         archive.map.values.clear();
     } else {
         // DDM_D2H_WIDEN=1 (f32 runs): the map stays f32 on the device and is widened on the

@@ -30,6 +30,8 @@ struct Ingest {
     double frame_interval = 1.0;
 };
 
+// ResultArchive::validate over n values (`archive.cpp:44-58`), same errors and precedence.
+void validate_values(const double* values, std::size_t n, bool f32);
 // write_partial with the payload from any host buffer (the run's own map when it is the
 // whole partial), written by several threads
 std::filesystem::path write_partial_payload(const PartialResult& header, const double* values,

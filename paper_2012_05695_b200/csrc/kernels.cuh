@@ -116,6 +116,11 @@ cudaError_t launch_pairwise(const void* spec, int N, int64_t nq, const int* lags
                             double* out, int64_t out_stride, const int64_t* dest_of_slot,
                             int num_sms, cudaStream_t stream, int lag0 = -1);
 
+// frame-major spectra [N][plane] -> wave-vector-major [count][N] at positions flat[k]
+template <typename S>
+cudaError_t launch_gather_sequences(const void* frames, int N, int64_t plane, const int64_t* flat,
+                                    int64_t count, void* seq, cudaStream_t stream);
+
 // Relaxation fits, one warp per ring (`analysis.cpp:108-224`): means [n_lags][nbins] f64;
 // flag 0 ok, 1 degenerate, 2 no_converge, -1 not fitted.
 cudaError_t launch_fit_rings(const double* means, const int64_t* lags, int n_lags,

@@ -143,9 +143,11 @@ cudaError_t launch_pairwise(const void* spec, int N, int64_t nq, const int* lags
     static const bool generic = std::getenv("DDM_PAIRWISE_GENERIC") != nullptr;   // A/B
     // a contiguous range of at least one full lag group (32 lanes x kLpl lags): shorter ranges
     // leave most lanes idle and stay on the one-lane-per-lag kernel
-    if (lag0 >= 0 && !generic && n_lags >= 32 * kLpl) {
-        const size_t smem = (size_t)(N + N / kLpl + 1) * sizeof(double2);
-        if (smem > 227 * 1024) return cudaErrorInvalidValue;
+    // The window buffer needs (N + N/kLpl + 1) values: past 227 KiB (N >= 11623) the
+    // one-lane-per-lag kernel serves the range too (it needs N values, up to N = 14528).
+    const size_t consec_smem = (size_t)(N + N / kLpl + 1) * sizeof(double2);
+    if (lag0 >= 0 && !generic && n_lags >= 32 * kLpl && consec_smem <= 227 * 1024) {
+        const size_t smem = consec_smem;
         auto k = pairwise_consec_kernel<S>;
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
@@ -173,6 +175,49 @@ cudaError_t launch_pairwise(const void* spec, int N, int64_t nq, const int* lags
                                                        n_lags, out, out_stride, dest_of_slot);
     return cudaGetLastError();
 }
+
+namespace {
+
+// frame-major spectra [N][plane] -> wave-vector-major sequences [count][N] of the retained
+// positions flat[k] (SpectrumStack -> the pairwise kernel's layout); 32 x 8 tiles through
+// shared memory so both sides are coalesced
+template <typename S>
+__global__ void gather_sequences_kernel(const cpx<S>* __restrict__ frames, int N, int64_t plane,
+                                        const int64_t* __restrict__ flat, int64_t count,
+                                        cpx<S>* __restrict__ seq) {
+    __shared__ cpx<S> tile[32][33];
+    const int64_t k0 = (int64_t)blockIdx.x * 32;
+    const int n0 = blockIdx.y * 32;
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    for (int j = ty; j < 32; j += 8) {
+        const int n = n0 + j;
+        const int64_t k = k0 + tx;
+        if (n < N && k < count) tile[j][tx] = frames[(int64_t)n * plane + flat[k]];
+    }
+    __syncthreads();
+    for (int j = ty; j < 32; j += 8) {
+        const int64_t k = k0 + j;
+        const int n = n0 + tx;
+        if (n < N && k < count) seq[k * N + n] = tile[tx][j];
+    }
+}
+
+}  // namespace
+
+template <typename S>
+cudaError_t launch_gather_sequences(const void* frames, int N, int64_t plane, const int64_t* flat,
+                                    int64_t count, void* seq, cudaStream_t stream) {
+    if (count == 0 || N == 0) return cudaSuccess;
+    dim3 grid((unsigned)((count + 31) / 32), (unsigned)((N + 31) / 32));
+    gather_sequences_kernel<S><<<grid, dim3(32, 8), 0, stream>>>(
+        static_cast<const cpx<S>*>(frames), N, plane, flat, count, static_cast<cpx<S>*>(seq));
+    return cudaGetLastError();
+}
+
+template cudaError_t launch_gather_sequences<float>(const void*, int, int64_t, const int64_t*, int64_t,
+                                                    void*, cudaStream_t);
+template cudaError_t launch_gather_sequences<double>(const void*, int, int64_t, const int64_t*, int64_t,
+                                                     void*, cudaStream_t);
 
 template cudaError_t launch_pairwise<float>(const void*, int, int64_t, const int*, int, double*,
                                             int64_t, const int64_t*, int, cudaStream_t, int);

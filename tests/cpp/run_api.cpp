@@ -47,7 +47,7 @@ int main(int argc, char** argv) {
     pw.algorithm = ddm::Algorithm::WithoutFt;
     const ddm::ResultArchive b = ddm::run(src, pw);
     EXPECT(b.counters.pairs == 96ull * 95 / 2);
-    EXPECT(ddm::relative_deviation(a.map, b.map) <= 1e-9);
+    EXPECT(ddm::b200::relative_deviation(a.map, b.map) <= 1e-9);
 
     const ddm::CompareReport r = ddm::compare(src, cfg, ddm::Algorithm::WithFt, ddm::Algorithm::WithoutFt);
     EXPECT(r.pass && r.tolerance == 1e-9 && r.algorithms[0] == "with_ft" && r.algorithms[1] == "without_ft");
@@ -55,7 +55,7 @@ int main(int argc, char** argv) {
     ddm::RunConfig f32 = cfg;
     f32.precision = ddm::Precision::F32;
     const ddm::ResultArchive c = ddm::analyze(src, f32, root / "out");
-    EXPECT(ddm::relative_deviation(a.map, c.map) <= 1e-4);
+    EXPECT(ddm::b200::relative_deviation(a.map, c.map) <= 1e-4);
     for (const char* f : {"index.json", "d_m0.bin", "d_m95.bin", "radial.csv", "fits.csv", "partials/group0.bin"})
         EXPECT(fs::exists(root / "out" / f));
     const ddm::ResultArchive back = ddm::read_results(root / "out");

@@ -78,12 +78,18 @@ def run_case(torch, D, W, H, N, seed, k=512, expect=()):
     for e in expect:
         assert e in eng, (e, eng)
     got = out.index_select(1, torch.as_tensor(idx, device="cuda")).cpu().numpy().astype(np.float64)
-    # whole-map properties at full size: d(0) == 0 exactly, finite, validate() floor
+    # whole-map properties at full size (lag chunks, no map-sized temporaries): d(0) == 0
+    # exactly, finite, the validate() floor (`archive.cpp:44-58`)
     assert bool(torch.all(out[0] == 0))
-    assert bool(torch.isfinite(out).all())
-    peak = float(out.max())
-    assert float(out.min()) >= -1e-4 * max(peak, 1.0)
+    peak, low = 0.0, 0.0
+    for l0 in range(0, N, 64):
+        blk = out[l0:l0 + 64]
+        assert bool(torch.isfinite(blk).all())
+        peak = max(peak, float(blk.max()))
+        low = min(low, float(blk.min()))
+    assert low >= -1e-4 * max(peak, 1.0)
     err = O.relative_l2(got, ref)
+    print(f"{W}x{H}x{N}: relative L2 {err:.3e} over {len(idx)} wave vectors [{eng}]")
     assert err <= F32_L2, (W, H, N, err, eng)
     return frames, out, err
 
