@@ -37,10 +37,30 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-W, H, N = 512, 512, 1024
 METRIC = "frames/s for 512×512×1024 d(q,m) at 1/2/4/8 B200; % HBM roofline"
 UNIT = "frames/s"
-WORKLOAD = "512x512 px x 1024 frames, WITH_FT d(q,m), all 131584 wave vectors x 1024 lags"
+# BASELINE.json configs: c2 is the metric's (default, what the driver runs); c3 / c4 are the
+# long-sequence shapes (`--config`), frames rendered on the device by the synthetic generator
+CONFIGS = {
+    "c2": (512, 512, 1024),
+    "c3": (1024, 1024, 2048),
+    "c4": (2048, 2048, 4096),
+}
+W, H, N = CONFIGS["c2"]
+CONFIG_NAME = "c2"
+
+
+def workload() -> str:
+    return (f"{W}x{H} px x {N} frames, WITH_FT d(q,m), all {H * (W // 2 + 1)} wave vectors x "
+            f"{N} lags")
+
+
+def config_dict() -> dict:
+    """The `config` both arms print (identical dicts: same workload, same precision)."""
+    return {"workload": workload(), "config": CONFIG_NAME, "width": W, "height": H, "frames": N,
+            "precision": "f32",
+            "frames_source": "ddm::generate (P=100, D=0.5, psf 1, seed 7)",
+            "l2": "no flush: inputs larger than L2 (frames, spectra and map are each > 126 MB)"}
 
 
 def peaks():
@@ -108,6 +128,15 @@ def synth_stack():
     return ddm.generate(W, H, N, particles=100, diffusion=0.5, seed=7)
 
 
+def device_stack(dev: int):
+    """The same frames rendered in HBM by the device generator (`ddm_b200_generate_device`)."""
+    import torch
+    from paper_2012_05695_b200 import ddm
+    t = torch.empty(N * H * W, dtype=torch.int16, device=f"cuda:{dev}")
+    ddm.generate_device(t.data_ptr(), W, H, N, particles=100, diffusion=0.5, seed=7, device=dev)
+    return t
+
+
 def traffic_from_profiles(stage: str):
     """DRAM bytes per launch of the stage's kernel from the latest committed ncu --set full
     capture (profiles/ncu_traffic.json, written by tools/profile_summary.py), or None."""
@@ -153,24 +182,30 @@ def reference_arm(args, rank: int):
         return
     st = ref.generate(W, H, N, particles=100, diffusion=0.5, seed=7)
     cores = host_cores()
-    times = []
+    totals, walls = [], []
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
         r = ref.run(st, "with_ft", "f32", memory_bytes=1 << 40, workers=cores)
         dt = time.perf_counter() - t0
         if i >= args.warmup:
-            times.append(dt)
-    ms = 1e3 * float(np.mean(times))
+            totals.append(r.timing["total"])
+            walls.append(dt)
+    # the reference's own TimingBreakdown.total of ddm::run (`scheduler.cpp:413-483`): the
+    # ctypes veneer's buffer copies (oracle/ref.py, ref_capi.cpp) are outside it
+    ms = 1e3 * float(np.mean(totals))
     value = N / (ms / 1e3)
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "width": W, "height": H, "frames": N, "precision": "f32"},
+        "config": config_dict(),
+        "wall": {"value": N / float(np.mean(walls)), "ms_per_step": 1e3 * float(np.mean(walls)),
+                 "what": "wall time of the wrapper call (adds the veneer's host copies)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
                          "sample": f"full workload per step: ddm::run(MemoryFrameSource, with_ft, "
                                    f"f32, workers={cores}) from oracle/_ref (reference core + "
-                                   f"FFTW-API shim), breakdown of last step {r.timing}"},
+                                   f"FFTW-API shim, not FFTW), timed by the reference's "
+                                   f"TimingBreakdown.total; breakdown of last step {r.timing}"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
@@ -178,19 +213,44 @@ def reference_arm(args, rank: int):
 # --------------------------------------------------------------------------- our arm
 
 def cpu_baseline_sample():
-    """The reference CPU path on this host, bounded: one full C2 run (~10-30 s)."""
+    """The reference CPU path on this host, bounded: one full C2 run (~10-30 s). Returns the
+    baseline entry and the reference's map (for the parity field)."""
     from oracle import ref
     if not ref.available():
-        return None
+        return None, None
     st = ref.generate(W, H, N, particles=100, diffusion=0.5, seed=7)
     cores = host_cores()
     t0 = time.perf_counter()
     r = ref.run(st, "with_ft", "f32", memory_bytes=1 << 40, workers=cores)
     dt = time.perf_counter() - t0
-    return {"value": N / dt, "unit": UNIT, "cores": cores, "kind": "reference",
-            "sample": f"one full 512x512x1024 f32 run of the reference ddm::run "
-                      f"(oracle/_ref: reference core + FFTW-API shim), {dt:.2f} s wall, "
-                      f"phases {json.dumps({k: round(v, 3) for k, v in r.timing.items()})}"}
+    tot = r.timing["total"]
+    return ({"value": N / tot, "unit": UNIT, "cores": cores, "kind": "reference",
+             "sample": f"one full {W}x{H}x{N} f32 run of the reference ddm::run (oracle/_ref: "
+                       f"reference core + FFTW-API shim), TimingBreakdown.total {tot:.2f} s "
+                       f"({dt:.2f} s wrapper wall), phases "
+                       f"{json.dumps({k: round(v, 3) for k, v in r.timing.items()})}"},
+            r.values.reshape(-1))
+
+
+def parity_vs_reference(ours: np.ndarray, ref_map) -> dict:
+    """North-star parity of the e2e map against the reference's own map of the same frames:
+    relative L2 (bound 1e-4 for f32) and max |a - b| / peak (`ddm_cli.cpp:132-141`)."""
+    if ref_map is None:
+        return None
+    a = np.asarray(ours, dtype=np.float64)
+    b = np.asarray(ref_map, dtype=np.float64)
+    num = den = 0.0
+    dmax = peak = 0.0
+    for i in range(0, a.size, 1 << 24):
+        d = a[i:i + (1 << 24)] - b[i:i + (1 << 24)]
+        num += float(d @ d)
+        den += float(b[i:i + (1 << 24)] @ b[i:i + (1 << 24)])
+        dmax = max(dmax, float(np.abs(d).max()))
+        peak = max(peak, float(np.abs(b[i:i + (1 << 24)]).max()), float(np.abs(a[i:i + (1 << 24)]).max()))
+    rel_l2 = (num / den) ** 0.5 if den > 0 else num ** 0.5
+    return {"against": "reference ddm::run f32 map (oracle/_ref), every entry", "entries": int(a.size),
+            "relative_l2": rel_l2, "max_abs_over_peak": dmax / peak if peak > 0 else dmax,
+            "bound_relative_l2": 1e-4, "pass": rel_l2 <= 1e-4}
 
 
 def shard_chunks(n: int) -> int:
@@ -215,12 +275,20 @@ def sharded_arm(args, rank: int, world: int):
         os.environ.setdefault("MASTER_PORT", "29533")
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev}"),
                                 rank=rank, world_size=world)
-    st = synth_stack()
     Q = H * (W // 2 + 1)
     plan = sharded.plan_shards(Q, N, world)
     f0, f1 = plan.frame_begin[rank], plan.frame_begin[rank + 1]
-    local_host = torch.from_numpy(st[f0:f1].copy().view(np.int16))
-    frames_d = local_host.to(f"cuda:{dev}")
+    if CONFIG_NAME == "c2":
+        st = synth_stack()
+        local_host = torch.from_numpy(st[f0:f1].copy().view(np.int16))
+        frames_d = local_host.to(f"cuda:{dev}")
+    else:
+        # c3 / c4: the frames are rendered in HBM; the rank keeps its shard
+        full = device_stack(dev)
+        frames_d = full[f0 * H * W:f1 * H * W].clone()
+        del full
+        torch.cuda.empty_cache()
+        local_host = None
     ops = sharded.DeviceOps(W, H, "f32", device=dev, timing=False)
     # corner turn fused into the column pass over NVLink (symmetric-memory receive buffers);
     # NCCL all-to-all when peer mappings are unavailable
@@ -279,21 +347,23 @@ def sharded_arm(args, rank: int, world: int):
     dist.all_reduce(stage, op=dist.ReduceOp.MAX)
     s_ms, x_ms, t_ms = (float(x) for x in stage.tolist())
 
-    # e2e: the rank's pinned host frames in, its f32 partial out, every step
-    host_frames = local_host.pin_memory()
-    host_part = torch.empty(run.out.numel(), dtype=torch.float32).pin_memory()
-    dist.barrier()
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    e2e_steps = max(3, min(args.steps, 10))
-    for _ in range(e2e_steps):
-        frames_d.copy_(host_frames, non_blocking=True)
-        run.step(frames_d)
-        host_part.copy_(run.out, non_blocking=True)
+    # e2e (c2): the rank's pinned host frames in, its f32 partial out, every step
+    e2e_s = None
+    if local_host is not None:
+        host_frames = local_host.pin_memory()
+        host_part = torch.empty(run.out.numel(), dtype=torch.float32).pin_memory()
+        dist.barrier()
         torch.cuda.synchronize()
-    e2e_s = torch.tensor([(time.perf_counter() - t0) / e2e_steps], device=f"cuda:{dev}")
-    dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
-    e2e_s = float(e2e_s.item())
+        t0 = time.perf_counter()
+        e2e_steps = max(3, min(args.steps, 10))
+        for _ in range(e2e_steps):
+            frames_d.copy_(host_frames, non_blocking=True)
+            run.step(frames_d)
+            host_part.copy_(run.out, non_blocking=True)
+            torch.cuda.synchronize()
+        e2e_s = torch.tensor([(time.perf_counter() - t0) / e2e_steps], device=f"cuda:{dev}")
+        dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+        e2e_s = float(e2e_s.item())
     if rank == 0:
         pk, pk_kind = peaks()
         q_r, n_r = plan.q_of(0), plan.frames_of(0)
@@ -306,11 +376,10 @@ def sharded_arm(args, rank: int, world: int):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "width": W, "height": H, "frames": N,
-                       "precision": "f32", "map_dtype": "f32, one lag-major partial per rank",
-                       "l2": "no flush: per-rank inputs larger than L2",
-                       "parallelism": f"sharded x{world}: frames for the spatial step, "
-                                      f"wave vectors for the temporal step, corner turn {mode}"},
+            "config": config_dict(),
+            "setup": {"map_dtype": "f32, one lag-major partial per rank",
+                      "parallelism": f"sharded x{world}: frames for the spatial step, "
+                                     f"wave vectors for the temporal step, corner turn {mode}"},
             "roofline": {"bound": "hbm", "kernel": dominant[0], "achieved": achieved,
                          "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": achieved / pk["hbm_gbs"],
                          "peak_kind": pk_kind, "traffic": None,
@@ -322,16 +391,76 @@ def sharded_arm(args, rank: int, world: int):
                        "exchange_GBps_per_rank": sent / ((x_ms if mode == "nccl" else s_ms + x_ms) / 1e3) / 1e9,
                        "nvlink_peak_GBps": 900.0},
             "clocks": clk.summary(),
-            "e2e": {"value": N / e2e_s, "unit": UNIT,
-                    "h2d_bytes_per_step": int(st.nbytes),
-                    "d2h_bytes_per_step": int(4 * N * Q), "ms_per_step": e2e_s * 1e3,
-                    "path": "per rank: pinned frame shard H2D, sharded pass, f32 partial D2H"},
+            "e2e": ({"value": N / e2e_s, "unit": UNIT,
+                     "h2d_bytes_per_step": int(2 * N * H * W),
+                     "d2h_bytes_per_step": int(4 * N * Q), "ms_per_step": e2e_s * 1e3,
+                     "path": "per rank: pinned frame shard H2D, sharded pass, f32 partial D2H"}
+                    if e2e_s is not None else
+                    {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+                     "unavailable": f"{CONFIG_NAME}: frames rendered on the device, no host leg"}),
             # per step: a row and a column pass per frame chunk of the shard (two chunks of
             # whole 16-frame column groups, Engine::spatial_pass) and one temporal launch
             "gpu_launches": args.steps * (2 * shard_chunks(n_r) + 1),
         }
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
+
+
+def e2e_leg(args, st, dev: int, plane: int):
+    """The metric end to end through the reference-facing C-ABI call `ddm_b200_run_u16`
+    (`ddm::run`): pinned host u16 frames in, the f64 lag-major ResultMap out, every call.
+    Returns the e2e entry and the host map of the last call."""
+    import ctypes as C
+
+    import torch
+    from paper_2012_05695_b200 import ddm
+    host_frames = torch.from_numpy(st).pin_memory()
+    host_map = torch.empty(N * plane, dtype=torch.float64).pin_memory()
+    cfg = ddm.RunConfig(precision="f32", memory_bytes=1 << 40, workers=1, device=dev)
+    keep = []
+    c = ddm._config(cfg, keep)
+    out_lags = np.zeros(N, dtype=np.int64)
+    n_lags = C.c_int64(0)
+    counters, timing = ddm.Counters(), ddm.Timing()
+
+    def e2e_step():
+        rc = ddm.lib().ddm_b200_run_u16(C.c_void_p(host_frames.data_ptr()), W, H, N,
+                                        C.c_double(1.0), C.byref(c),
+                                        C.c_void_p(host_map.data_ptr()), C.c_int64(N * plane),
+                                        ddm._p(out_lags, C.c_int64), C.byref(n_lags),
+                                        C.byref(counters), C.byref(timing))
+        ddm._check(rc)
+
+    for _ in range(max(3, args.warmup)):
+        e2e_step()
+    e2e_steps = max(5, min(args.steps, 20))
+    torch.cuda.synchronize()
+    phases = []
+    step_wall = []
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        ts = time.perf_counter()
+        e2e_step()
+        step_wall.append(time.perf_counter() - ts)
+        phases.append({f: float(getattr(timing, f)) for f, _ in ddm.Timing._fields_})
+    torch.cuda.synchronize()
+    e2e_mean_s = (time.perf_counter() - t0) / e2e_steps
+    # per-call wall time: the median step. Host-side stalls of a few hundred ms hit single
+    # calls on reused boxes (measured: one 507 ms step among 32 ms ones); the mean and the
+    # per-step list are reported beside it.
+    e2e_s = statistics.median(step_wall)
+    # the reference's TimingBreakdown of the C-ABI call, medians over the e2e steps (seconds):
+    # disk = pinned frames H2D, step1/step2 = device kernels, merge = f64 map D2H
+    e2e_phases = {f: statistics.median(p[f] for p in phases) for f in phases[0]}
+    h2d_gbps = st.nbytes / max(e2e_phases["disk"], 1e-9) / 1e9
+    d2h_gbps = N * plane * 8 / max(e2e_phases["merge"], 1e-9) / 1e9
+    e2e = {"value": N / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(st.nbytes),
+           "d2h_bytes_per_step": int(N * plane * 8), "ms_per_step": e2e_s * 1e3,
+           "phases_s": e2e_phases, "h2d_GBps": h2d_gbps, "d2h_GBps": d2h_gbps,
+           "path": "ddm_b200_run_u16 (C-ABI ddm::run): pinned u16 in, f64 lag-major map out",
+           "step_ms": [round(t * 1e3, 2) for t in step_wall],
+           "mean_ms_per_step": e2e_mean_s * 1e3, "estimator": "median over the e2e steps"}
+    return e2e, host_map.numpy()
 
 
 def our_arm(args, rank: int, world: int):
@@ -344,9 +473,13 @@ def our_arm(args, rank: int, world: int):
     torch.cuda.set_device(dev)
     dist = None
 
-    st = synth_stack()
     plane = H * (W // 2 + 1)
-    frames_d = torch.from_numpy(st.view(np.uint8).reshape(-1)).to(f"cuda:{dev}")
+    if CONFIG_NAME == "c2":
+        st = synth_stack()
+        frames_d = torch.from_numpy(st.view(np.uint8).reshape(-1)).to(f"cuda:{dev}")
+    else:
+        st = None                  # c3 / c4: rendered in HBM by the device generator
+        frames_d = device_stack(dev)
     out_d = torch.empty(N * plane, dtype=torch.float32, device=f"cuda:{dev}")
     stream = torch.cuda.current_stream()
 
@@ -397,51 +530,10 @@ def our_arm(args, rank: int, world: int):
         if dist:
             dist.destroy_process_group()
         return
-    host_frames = torch.from_numpy(st).pin_memory()
-    host_map = torch.empty(N * plane, dtype=torch.float64).pin_memory()
-    cfg = ddm.RunConfig(precision="f32", memory_bytes=1 << 40, workers=1, device=dev)
-    import ctypes as C
-    keep = []
-    c = ddm._config(cfg, keep)
-    out_lags = np.zeros(N, dtype=np.int64)
-    n_lags = C.c_int64(0)
-    counters, timing = ddm.Counters(), ddm.Timing()
-
-    def e2e_step():
-        rc = ddm.lib().ddm_b200_run_u16(C.c_void_p(host_frames.data_ptr()), W, H, N,
-                                        C.c_double(1.0), C.byref(c),
-                                        C.c_void_p(host_map.data_ptr()), C.c_int64(N * plane),
-                                        ddm._p(out_lags, C.c_int64), C.byref(n_lags),
-                                        C.byref(counters), C.byref(timing))
-        ddm._check(rc)
-
-    for _ in range(max(3, args.warmup)):
-        e2e_step()
-    e2e_steps = max(5, min(args.steps, 20))
-    torch.cuda.synchronize()
-    phases = []
-    step_wall = []
-    t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        ts = time.perf_counter()
-        e2e_step()
-        step_wall.append(time.perf_counter() - ts)
-        phases.append({f: float(getattr(timing, f)) for f, _ in ddm.Timing._fields_})
-    torch.cuda.synchronize()
-    e2e_mean_s = (time.perf_counter() - t0) / e2e_steps
-    # per-call wall time: the median step. Host-side stalls of a few hundred ms hit single
-    # calls on reused boxes (measured: one 507 ms step among 32 ms ones); the mean and the
-    # per-step list are reported beside it.
-    e2e_s = statistics.median(step_wall)
-    # the reference's TimingBreakdown of the C-ABI call, medians over the e2e steps (seconds):
-    # disk = pinned frames H2D, step1/step2 = device kernels, merge = f64 map D2H
-    e2e_phases = {f: statistics.median(p[f] for p in phases) for f in phases[0]}
-    h2d_gbps = st.nbytes / max(e2e_phases["disk"], 1e-9) / 1e9
-    d2h_gbps = N * plane * 8 / max(e2e_phases["merge"], 1e-9) / 1e9
-    if dist:
-        t = torch.tensor([e2e_s], device=f"cuda:{dev}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+    e2e, host_map = (e2e_leg(args, st, dev, plane) if st is not None else
+                     ({"value": None, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+                       "unavailable": f"{CONFIG_NAME}: frames rendered on the device; the f64 "
+                                      f"host map would be {N * plane * 8 / 1e9:.0f} GB"}, None))
 
     if rank != 0:
         if dist:
@@ -462,11 +554,9 @@ def our_arm(args, rank: int, world: int):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "width": W, "height": H, "frames": N, "precision": "f32",
-                   "map_dtype": "f32 (value) / f64 (e2e, reference ResultMap)",
-                   "l2": "no flush: inputs larger than L2 (0.5 GiB frames, 1.0 GiB spectra, "
-                         "0.5 GiB map per step vs 126 MB L2)",
-                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+        "config": config_dict(),
+        "setup": {"map_dtype": "f32 (value) / f64 (e2e, reference ResultMap)",
+                  "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
         "roofline": {"bound": "hbm", "kernel": dominant[0], "achieved": achieved,
                      "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": achieved / pk["hbm_gbs"],
                      "peak_kind": pk_kind,
@@ -480,16 +570,13 @@ def our_arm(args, rank: int, world: int):
                    "pipeline_GBps": total_bytes / (ms / 1e3) / 1e9,
                    "pipeline_frac_of_hbm": total_bytes / (ms / 1e3) / 1e9 / pk["hbm_gbs"]},
         "clocks": clk_now,
-        "e2e": {"value": world * N / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(st.nbytes),
-                "d2h_bytes_per_step": int(N * plane * 8), "ms_per_step": e2e_s * 1e3,
-                "phases_s": e2e_phases, "h2d_GBps": h2d_gbps, "d2h_GBps": d2h_gbps,
-                "path": "ddm_b200_run_u16 (C-ABI ddm::run): pinned u16 in, f64 lag-major map out",
-                "step_ms": [round(t * 1e3, 2) for t in step_wall],
-                "mean_ms_per_step": e2e_mean_s * 1e3, "estimator": "median over the e2e steps"},
+        "e2e": e2e,
         "gpu_launches": launches,
     }
-    if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline_sample()
+    if world == 1 and not args.no_cpu_baseline and CONFIG_NAME == "c2":
+        line["cpu_baseline"], ref_map = cpu_baseline_sample()
+        if host_map is not None:
+            line["parity"] = parity_vs_reference(host_map, ref_map)
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
@@ -507,7 +594,12 @@ def main():
                     help="run the sharded multi-GPU pass even on one rank (exercises the path)")
     ap.add_argument("--no-e2e", action="store_true",
                     help="skip the C-ABI host-buffer leg (profiling runs)")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c2",
+                    help="BASELINE workload: c2 (the metric's, default), c3, c4")
     args = ap.parse_args()
+    global W, H, N, CONFIG_NAME
+    W, H, N = CONFIGS[args.config]
+    CONFIG_NAME = args.config
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     if args.impl == "reference":

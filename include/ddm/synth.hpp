@@ -27,6 +27,13 @@ struct SynthConfig {
 
 ImageStack generate(const SynthConfig& config);
 
+/// The same stack rendered on the device into d_out ([frames][height][width] u16 in HBM,
+/// b200 extension): trajectories from the reference's draw sequence on the host, frames by
+/// the render kernel (csrc/synth.cu) with the reference's per-pixel addition order. Ordered
+/// after `stream` (cudaStream_t, may be null); returns when the frames are written.
+void generate_device(const SynthConfig& config, std::uint16_t* d_out, int device = 0,
+                     void* stream = nullptr);
+
 /// synth.json beside a generated stack (`synth.cpp:134-155`): tool version, generator name and
 /// every SynthConfig field.
 void write_synth_manifest(const SynthConfig& config, const std::filesystem::path& path);

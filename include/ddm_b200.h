@@ -272,6 +272,14 @@ int ddm_b200_estimate_diffusion(const double* tau, const int* flag, int64_t nbin
 int ddm_b200_generate(int64_t particles, double diffusion, double psf_sigma, double amplitude,
                       double background, int width, int height, int frames,
                       double frame_interval, uint64_t seed, uint16_t* out);
+/* The same frames rendered on the device into d_out ([frames][height][width] u16 in HBM):
+   the generator staging frames to HBM (BASELINE north_star). Trajectories on the host with
+   the reference's draw sequence; frames by a render kernel with the reference's per-pixel
+   arithmetic (synth.cpp:42-79). Ordered after `stream`; returns when the frames are written. */
+int ddm_b200_generate_device(int64_t particles, double diffusion, double psf_sigma,
+                             double amplitude, double background, int width, int height,
+                             int frames, double frame_interval, uint64_t seed, uint16_t* d_out,
+                             int device, void* stream);
 
 #ifdef __cplusplus
 }

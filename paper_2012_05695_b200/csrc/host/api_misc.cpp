@@ -320,19 +320,14 @@ void splat(const std::vector<double>& xs, const std::vector<double>& ys, const S
     }
 }
 
-}  // namespace
-
-ImageStack generate(const SynthConfig& c) {
-    c.validate();
-    ImageStack st;
-    st.width = c.width;
-    st.height = c.height;
-    st.frames = c.frames;
-    st.frame_interval = c.frame_interval;
-    st.pixels.resize(std::size_t(c.frames) * std::size_t(st.pixels_per_frame()));
-    std::mt19937_64 g(c.seed);
+// Particle positions of every frame, [frames][particles][2] (x, y): the reference's draw
+// sequence (`synth.cpp:98-132`): uniform starts, then per frame and particle one Box-Muller
+// pair, periodic wrap.
+std::vector<double> trajectories(const SynthConfig& c) {
     const auto np = std::size_t(c.particles);
-    std::vector<double> xs(np), ys(np), canvas;
+    std::vector<double> pos(std::size_t(c.frames) * np * 2);
+    std::mt19937_64 g(c.seed);
+    std::vector<double> xs(np), ys(np);
     for (std::size_t p = 0; p < np; ++p) {
         xs[p] = draw01(g) * c.width;
         ys[p] = draw01(g) * c.height;
@@ -351,9 +346,63 @@ ImageStack generate(const SynthConfig& c) {
                 ys[p] = periodic(ys[p] + step * (rad * std::sin(th)), c.height);
             }
         }
+        double* f = pos.data() + std::size_t(n) * np * 2;
+        for (std::size_t p = 0; p < np; ++p) {
+            f[2 * p] = xs[p];
+            f[2 * p + 1] = ys[p];
+        }
+    }
+    return pos;
+}
+
+}  // namespace
+
+ImageStack generate(const SynthConfig& c) {
+    c.validate();
+    ImageStack st;
+    st.width = c.width;
+    st.height = c.height;
+    st.frames = c.frames;
+    st.frame_interval = c.frame_interval;
+    st.pixels.resize(std::size_t(c.frames) * std::size_t(st.pixels_per_frame()));
+    const auto np = std::size_t(c.particles);
+    const std::vector<double> pos = trajectories(c);
+    std::vector<double> xs(np), ys(np), canvas;
+    for (int n = 0; n < c.frames; ++n) {
+        const double* f = pos.data() + std::size_t(n) * np * 2;
+        for (std::size_t p = 0; p < np; ++p) {
+            xs[p] = f[2 * p];
+            ys[p] = f[2 * p + 1];
+        }
         splat(xs, ys, c, st.frame(n).data(), canvas);
     }
     return st;
+}
+
+void generate_device(const SynthConfig& c, std::uint16_t* d_out, int device, void* stream) {
+    c.validate();
+    if (!d_out) throw InputError("null device buffer");
+    const std::vector<double> pos = trajectories(c);
+    detail::guard_device([&] {
+        b200::Engine& eng = b200::Engine::instance(device);
+        std::lock_guard<std::mutex> lock(eng.mutex());
+        cudaStream_t st = eng.stream();
+        cudaEvent_t ev;
+        b200::check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+        b200::check(cudaEventRecord(ev, static_cast<cudaStream_t>(stream)), "event record");
+        b200::check(cudaStreamWaitEvent(st, ev, 0), "stream wait");
+        void* d_pos = eng.buffer("synth_pos", std::max<std::size_t>(pos.size(), 1) * sizeof(double));
+        b200::check(cudaMemcpyAsync(d_pos, pos.data(), pos.size() * sizeof(double), cudaMemcpyHostToDevice, st),
+                    "upload");
+        b200::check(ddmk::launch_render_frames(static_cast<const double*>(d_pos), int(c.particles), c.width,
+                                               c.height, c.frames, c.psf_sigma, c.amplitude, c.background,
+                                               d_out, st), "render kernel");
+        b200::check(cudaEventRecord(ev, st), "event record");
+        b200::check(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), ev, 0), "stream wait");
+        b200::check(cudaStreamSynchronize(st), "sync");   // `pos` is host memory
+        cudaEventDestroy(ev);
+        return 0;
+    });
 }
 
 void write_synth_manifest(const SynthConfig& c, const std::filesystem::path& path) {

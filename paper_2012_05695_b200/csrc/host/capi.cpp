@@ -921,4 +921,24 @@ int ddm_b200_generate(int64_t particles, double diffusion, double psf_sigma, dou
     });
 }
 
+int ddm_b200_generate_device(int64_t particles, double diffusion, double psf_sigma,
+                             double amplitude, double background, int width, int height,
+                             int frames, double frame_interval, uint64_t seed, uint16_t* d_out,
+                             int device, void* stream) {
+    return guarded([&] {
+        ddm::SynthConfig c;
+        c.particles = particles;
+        c.diffusion = diffusion;
+        c.psf_sigma = psf_sigma;
+        c.amplitude = amplitude;
+        c.background = background;
+        c.width = width;
+        c.height = height;
+        c.frames = frames;
+        c.frame_interval = frame_interval;
+        c.seed = seed;
+        ddm::generate_device(c, d_out, device, stream);
+    });
+}
+
 }  // extern "C"

@@ -116,6 +116,12 @@ cudaError_t launch_pairwise(const void* spec, int N, int64_t nq, const int* lags
                             double* out, int64_t out_stride, const int64_t* dest_of_slot,
                             int num_sms, cudaStream_t stream, int lag0 = -1);
 
+// Synthetic frames (csrc/synth.cu): d_pos [frames][particles][2] particle positions ->
+// d_out [frames][H][W] u16, the reference's `render_frame` arithmetic (`synth.cpp:42-79`).
+cudaError_t launch_render_frames(const double* d_pos, int particles, int W, int H, int frames,
+                                 double psf_sigma, double amplitude, double background,
+                                 uint16_t* d_out, cudaStream_t stream);
+
 // frame-major spectra [N][plane] -> wave-vector-major [count][N] at positions flat[k]
 template <typename S>
 cudaError_t launch_gather_sequences(const void* frames, int N, int64_t plane, const int64_t* flat,

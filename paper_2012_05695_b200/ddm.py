@@ -602,6 +602,18 @@ def generate(width=64, height=64, frames=256, particles=100, diffusion=0.5, psf_
     return out
 
 
+def generate_device(out_ptr: int, width=64, height=64, frames=256, particles=100, diffusion=0.5,
+                    psf_sigma=1.0, amplitude=1000.0, background=100.0, frame_interval=1.0, seed=0,
+                    device: int = 0, stream: int = 0) -> None:
+    """ddm::generate rendered on the device into out_ptr ([frames][height][width] u16 in HBM,
+    e.g. a torch tensor's data_ptr); the trajectories are the reference's draw sequence."""
+    _check(lib().ddm_b200_generate_device(C.c_int64(particles), C.c_double(diffusion),
+                                          C.c_double(psf_sigma), C.c_double(amplitude),
+                                          C.c_double(background), width, height, frames,
+                                          C.c_double(frame_interval), C.c_uint64(seed),
+                                          C.c_void_p(out_ptr), device, C.c_void_p(stream)))
+
+
 def run_device(frames_ptr: int, pixel_bytes: int, width: int, height: int, frames: int,
                out_ptr: int, precision: str = "f32", out_f64: bool = False, lags=None,
                q_max: Optional[float] = None, device: int = 0, stream: int = 0,
