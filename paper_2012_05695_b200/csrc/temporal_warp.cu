@@ -90,6 +90,8 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
     // 16-byte vector stores of whole tiles: f32 map, aligned base and row stride
     const bool vec_store = sizeof(OutT) == 4 && kWarps % 4 == 0 &&
                            ((uintptr_t)out & 15) == 0 && (out_stride & 3) == 0;
+    // f64 map (the reference's ResultMap): 16-byte stores of wave-vector pairs
+    const bool vec_store2 = sizeof(OutT) == 8 && ((uintptr_t)out & 15) == 0 && (out_stride & 1) == 0;
     __syncthreads();
 
     const int64_t ntiles = (nq + kWarps - 1) / kWarps;
@@ -327,6 +329,23 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
                     v4.z = ws[4 * h + 2].pw[padded(m)];
                     v4.w = ws[4 * h + 3].pw[padded(m)];
                     *reinterpret_cast<float4*>(pdst) = v4;
+                }
+            } else if (vec_store2) {
+                // quads of threads cover one lag row's kWarps * 8 = 64-byte run: thread 4i + k
+                // stores wave vectors 2k, 2k + 1 as one double2, so a store instruction
+                // writes 8 whole rows (16 full 32-byte sectors); the pw reads stay
+                // conflict-free (WarpSmem is 4 banks apart per warp)
+                static_assert(kWarps == 8, "quad store assumes 8 wave vectors per tile");
+                const int k = threadIdx.x & 3;
+                const int rows = blockDim.x >> 2;
+                OutT* pdst = out + (int64_t)(threadIdx.x >> 2) * out_stride + q0 + 2 * k;
+                const int64_t pstep = (int64_t)rows * out_stride;
+#pragma unroll 4
+                for (int m = threadIdx.x >> 2; m < N; m += rows, pdst += pstep) {
+                    double2 v2;
+                    v2.x = (double)ws[2 * k].pw[padded(m)];
+                    v2.y = (double)ws[2 * k + 1].pw[padded(m)];
+                    *reinterpret_cast<double2*>(pdst) = v2;
                 }
             } else {
                 for (int m = threadIdx.x; m < N; m += blockDim.x, dst += step) {
