@@ -46,6 +46,12 @@ __device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t b
         : "memory");
 }
 
+// one-instruction L2 prefetch of a contiguous range by the bulk-copy engine (16-byte aligned,
+// size a multiple of 16)
+__device__ __forceinline__ void l2_prefetch(const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 // wait with backoff: a warp whose copy has not landed sleeps between polls instead of
 // taking issue slots from the warps that have work
 __device__ __forceinline__ void mbar_wait_backoff(unsigned long long* bar, uint32_t phase) {

@@ -14,11 +14,19 @@
 // so it is formed with a pairwise f32 sum; everything the reference keeps in f64 (power,
 // averages term, combination) stays f64.
 //
-// Data movement per sequence: one TMA bulk copy (cp.async.bulk, 8 KB) into the warp's stage
-// buffer, issued one tile ahead; three four-step FFTs (warp_fft.cuh, one shared-memory
-// exchange each, the stage buffer doubles as scratch); the unfold reads U(L-m) from the
-// mirrored lane with shuffles; d(m) goes to the warp's D array and a CTA of 8 warps stores
-// 8 consecutive wave vectors per lag row.
+// Data movement per sequence: one TMA bulk copy (cp.async.bulk, 8 KB) into the warp's stage,
+// which stays resident through all three transforms (the odd transform re-reads it, the
+// averages term reads |t|^2 from it after the inverse); the next sequence's copy is issued
+// right after that, so it lands during the unfold and the tile store (an L2 prefetch of the
+// same bytes goes out one sequence earlier). Three four-step FFTs (warp_fft.cuh, one
+// shared-memory exchange each); the exchange buffer then holds |t|^2, S(m) and d(m); the
+// unfold reads U(L-m) from the mirrored lane with shuffles; a CTA of 12 warps stores 12
+// consecutive wave vectors per lag row.
+//
+// Occupancy: 12 warps per SM at <= 168 registers (218 KB of shared memory). The per-lane
+// unfold twiddles W_N2^{-(lane + 32 d)} are loop invariants the compiler would otherwise
+// keep in 64 registers for the kernel's life; they are formed per sequence from an opaque
+// copy of the lane base.
 #include <algorithm>
 #include <cstdlib>
 
@@ -39,14 +47,14 @@ constexpr int kPad = kL + kL / 32;    // slots per buffer (FFT scratch pitch 33 
 
 __device__ __forceinline__ int padded(int n) { return n + (n >> 5); }
 
-// Per-warp shared memory (16.9 KB; 12 warps + the reciprocal table fit one SM):
-//   stage   : TMA target of the sequence (dense [0, N) complex), re-read for the odd
-//             transform, then reused as f32 work space for |t|^2 and S(m)
-//   scratch : exchange buffer of the three FFTs, then the f32 lag values of the tile store
+// Per-warp shared memory (16.5 KB):
+//   stage   : TMA target of the sequence (dense [0, N) complex), read by the even and odd
+//             transforms and the averages term
+//   scratch : exchange buffer of the three FFTs; then, as f32 at padded(n): |t|^2, S(m) in
+//             place, d(m) in place (the tile store's source in map mode)
 struct WarpSmem {
-    cpx<float> stage[kPad];
+    cpx<float> stage[kL];
     cpx<float> scratch[kXS];     // FFT exchange (pitch kXP)
-    float pw[kPad];              // |t|^2, then S(m): frees the stage for the next copy early
     unsigned long long bar;
     unsigned long long pad_;
 };
@@ -87,11 +95,9 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
         base_unf = {(float)cs, (float)sn};
     }
     const float inv_nf = 1.0f / (float)N;
-    // 16-byte vector stores of whole tiles: f32 map, aligned base and row stride
-    const bool vec_store = sizeof(OutT) == 4 && kWarps % 4 == 0 &&
-                           ((uintptr_t)out & 15) == 0 && (out_stride & 3) == 0;
-    // f64 map (the reference's ResultMap): 16-byte stores of wave-vector pairs
-    const bool vec_store2 = sizeof(OutT) == 8 && ((uintptr_t)out & 15) == 0 && (out_stride & 1) == 0;
+    // 16-byte vector stores of whole tiles: aligned base and row stride (f32 map, or the f64
+    // map of the reference's ResultMap)
+    const bool vec_store = ((uintptr_t)out & 15) == 0 && (out_stride % (16 / (int)sizeof(OutT))) == 0;
     __syncthreads();
 
     const int64_t ntiles = (nq + kWarps - 1) / kWarps;
@@ -110,15 +116,28 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
         }
     };
 
+    // L2 prefetch of a sequence whose bulk copy is issued one sequence later
+    auto prefetch_l2 = [&](int64_t q) {
+        if (lane == 0 && q >= 0) {
+            if (segs.count == 0) {
+                l2_prefetch(spec + q * (int64_t)N, bytes);
+            } else {
+                for (int s = 0; s < segs.count; ++s)
+                    l2_prefetch(spec + segs.base[s] + q * (int64_t)segs.n[s], (uint32_t)segs.n[s] * 8u);
+            }
+        }
+    };
+
     auto tile_q = [&](int64_t tile) -> int64_t {
         const int64_t q = tile * kWarps + warp;
         return (tile < ntiles && q < nq) ? q : -1;
     };
 
     uint32_t phase = 0u;
-    // One sequence: wait for its copy, transform, call after_reload() once the stage is free
-    // (to start the next copy), emit(m, d(m)) for every m < N.
-    auto process = [&](int64_t q, bool live, auto&& after_reload, auto&& emit) {
+    float* sw = reinterpret_cast<float*>(my.scratch);   // the exchange buffer as f32 work space
+    // One sequence: wait for its copy, transform, call after_stage() once the stage has been
+    // read for the last time (to start the next copy), emit(m, d(m)) for every m < N.
+    auto process = [&](int64_t q, bool live, auto&& after_stage, auto&& emit) {
         if (live) {
             if (kBackoff) mbar_wait_backoff(&my.bar, phase);
             else mbar_wait(&my.bar, phase);
@@ -165,6 +184,10 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
             }
         }
 
+        // map mode: the previous tile's d values sit in every warp's exchange buffer until
+        // the CTA has stored them; the store overlaps this sequence's copy wait and mean
+        if constexpr (!kRing) __syncthreads();
+
         // ---- even outputs of the zero-padded FFT_2048: FFT_1024(t); P in f32 (`temporal.cpp:60-64`),
         //      kept in registers while the odd half is transformed
         float pe[32];
@@ -172,7 +195,7 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
 #pragma unroll
         for (int d = 0; d < 32; ++d) pe[d] = v[d].x * v[d].x + v[d].y * v[d].y;
 
-        // ---- odd outputs: reload t, keep |t|^2 (f32) in the stage for the averages term
+        // ---- odd outputs: t again from the stage
 #pragma unroll
         for (int b = 0; b < 32; ++b) {
             const int n = lane + 32 * b;
@@ -183,21 +206,27 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
             }
             v[b] = x;
         }
-        __syncwarp();
-        // the stage is free: start the next sequence's copy (it lands during three FFTs)
-        after_reload();
-        // map mode: the previous tile's d values wait in every warp's pw until the CTA has
-        // stored them; the store overlaps this sequence's mean and even transform
-        if constexpr (!kRing) __syncthreads();
-#pragma unroll
-        for (int b = 0; b < 32; ++b)
-            my.pw[padded(lane + 32 * b)] = v[b].x * v[b].x + v[b].y * v[b].y;
         fft1024<-1, true>(v, my.scratch, lane, tw_odd);
 #pragma unroll
         for (int d = 0; d < 32; ++d) v[d] = {pe[d], v[d].x * v[d].x + v[d].y * v[d].y};
 
         // ---- half-length inverse: lane c holds U[c + 32 d] in v[d]
         fft1024<+1, false>(v, my.scratch, lane, tw_even);
+
+        // ---- |t|^2 (f32, of the shifted sequence) from the stage into the now free exchange
+        //      buffer; then the stage is free: start the next sequence's copy
+#pragma unroll
+        for (int b = 0; b < 32; ++b) {
+            const int n = lane + 32 * b;
+            cpx<float> x = (live && n < N) ? my.stage[n] : cpx<float>{0.f, 0.f};
+            if (n < N) {
+                x.x -= mx;
+                x.y -= my_;
+            }
+            sw[padded(n)] = x.x * x.x + x.y * x.y;
+        }
+        __syncwarp();
+        after_stage();
 
         // ---- S(m) = sum_{n >= m} (p_n + p_{N-1-n}) = (N - m) d_a(m)  (`temporal.cpp:19-42`):
         //      lane a scans n = 32 a + j in f32, lane totals are suffix-summed in f64
@@ -207,7 +236,7 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
                 const int n = 32 * lane + j;
-                qv[j] = (n < N) ? my.pw[padded(n)] + my.pw[padded(N - 1 - n)] : 0.f;
+                qv[j] = (n < N) ? sw[padded(n)] + sw[padded(N - 1 - n)] : 0.f;
             }
             float r = 0.f;
 #pragma unroll
@@ -223,7 +252,7 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
             }
             const float base = (float)(incl - (double)r);
             __syncwarp();
-            float* sarea = my.pw;  // S(m) replaces |t|^2
+            float* sarea = sw;  // S(m) replaces |t|^2
 #pragma unroll
             for (int j = 0; j < 32; ++j) sarea[padded(32 * lane + j)] = qv[j] + base;
             __syncwarp();
@@ -237,6 +266,11 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
         //      2 Re R(m) = (A.x + B.x) + w.x (A.y + B.y) + w.y (A.x - B.x), w = W_N2^{-m}
         //      d(m) = (S(m) - 2 corr(m)) / (N - m), 2 corr(m) = 2 Re R(m) / N2
         const int src = (32 - lane) & 31;
+        // opaque per-sequence copy of the lane base: stops the compiler from hoisting the 32
+        // products base * W_N2^{-32 d} out of the sequence loop (64 registers)
+        cpx<float> bu;
+        asm volatile("mov.b32 %0, %1;" : "=f"(bu.x) : "f"(base_unf.x));
+        asm volatile("mov.b32 %0, %1;" : "=f"(bu.y) : "f"(base_unf.y));
         constexpr float inv_n2 = 1.0f / (float)kN2;
 #pragma unroll
         for (int d = 0; d < 32; ++d) {
@@ -246,7 +280,7 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
             Bc.y = __shfl_sync(0xffffffffu, v[31 - d].y, src);
             if (lane == 0) Bc = v[(32 - d) & 31];
             const cpx<float> A = v[d];
-            const cpx<float> w = cmul(base_unf, ct_w<+1, float>(32 * d, kN2));  // exp(+2 pi i m / N2)
+            const cpx<float> w = cmul(bu, ct_w<+1, float>(32 * d, kN2));  // exp(+2 pi i m / N2)
             const float re2 = (A.x + Bc.x) + (w.x * (A.y + Bc.y) + w.y * (A.x - Bc.x));
             if (m < N) {
                 const float val = fmaf(-re2, inv_n2, sv[d]) * rcp[m];
@@ -279,11 +313,9 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
 #pragma unroll
             for (int d = 0; d < 32; ++d) acc[padded(lane + 32 * d)] = 0.f;
             for (int64_t i = beg + warp; i < end; i += kWarps) {
-                process(ring.order[i], true,
-                        [&] {
-                            pi = (i + kWarps < end) ? i + kWarps : first_from(it + gridDim.x);
-                            prefetch_q(pi >= 0 ? ring.order[pi] : -1);
-                        },
+                pi = (i + kWarps < end) ? i + kWarps : first_from(it + gridDim.x);
+                prefetch_l2(pi >= 0 ? ring.order[pi] : -1);
+                process(ring.order[i], true, [&] { prefetch_q(pi >= 0 ? ring.order[pi] : -1); },
                         [&](int m, float val) { acc[padded(m)] += val; });
             }
             __syncthreads();
@@ -303,55 +335,51 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int64_t q = tile * kWarps + warp;
         const bool live = q < nq;
+        prefetch_l2(tile_q(tile + gridDim.x));
         process(q, live, [&] { prefetch_q(tile_q(tile + gridDim.x)); },
-                [&](int m, float val) { my.pw[padded(m)] = val; });   // S(m) was read into sv
+                [&](int m, float val) { sw[padded(m)] = val; });   // S(m) was read into sv
 
-        // ---- tile store: lag rows of kWarps consecutive wave vectors (32 B runs for f32)
+        // ---- tile store: lag rows of kWarps consecutive wave vectors
         __syncthreads();
+        auto dval = [&](int j, int m) -> float {
+            return reinterpret_cast<const float*>(ws[j].scratch)[padded(m)];
+        };
         const int64_t q0 = tile * kWarps;
         if (!lag_index && !dest_of_slot && q0 + kWarps <= nq) {
             OutT* dst = out + (int64_t)threadIdx.x * out_stride + q0;
             const int64_t step = (int64_t)blockDim.x * out_stride;
             if (vec_store) {
-                // thread pairs cover one lag row's kWarps * 4 = 32-byte run: lane 2i stores
-                // warps 0-3, lane 2i+1 warps 4-7, so each store instruction is 16 full
-                // 32-byte requests instead of 32 half ones
-                static_assert(kWarps == 8, "pair store assumes 8 wave vectors per tile");
-                const int h = threadIdx.x & 1;
-                const int rows = blockDim.x >> 1;
-                OutT* pdst = out + (int64_t)(threadIdx.x >> 1) * out_stride + q0 + 4 * h;
+                // TPR threads cover one lag row's run of kWarps values (48 B f32 / 96 B f64 at
+                // 12 warps), each storing VPT consecutive wave vectors as one 16-byte vector:
+                // a store instruction writes whole rows instead of one value per row
+                constexpr int VPT = 16 / (int)sizeof(OutT);
+                constexpr int TPR = kWarps / VPT;
+                static_assert(kWarps % VPT == 0, "whole 16-byte vectors per row");
+                const int k = threadIdx.x % TPR;
+                const int rows = blockDim.x / TPR;
+                OutT* pdst = out + (int64_t)(threadIdx.x / TPR) * out_stride + q0 + VPT * k;
                 const int64_t pstep = (int64_t)rows * out_stride;
 #pragma unroll 4
-                for (int m = threadIdx.x >> 1; m < N; m += rows, pdst += pstep) {
-                    float4 v4;
-                    v4.x = ws[4 * h + 0].pw[padded(m)];
-                    v4.y = ws[4 * h + 1].pw[padded(m)];
-                    v4.z = ws[4 * h + 2].pw[padded(m)];
-                    v4.w = ws[4 * h + 3].pw[padded(m)];
-                    *reinterpret_cast<float4*>(pdst) = v4;
-                }
-            } else if (vec_store2) {
-                // quads of threads cover one lag row's kWarps * 8 = 64-byte run: thread 4i + k
-                // stores wave vectors 2k, 2k + 1 as one double2, so a store instruction
-                // writes 8 whole rows (16 full 32-byte sectors); the pw reads stay
-                // conflict-free (WarpSmem is 4 banks apart per warp)
-                static_assert(kWarps == 8, "quad store assumes 8 wave vectors per tile");
-                const int k = threadIdx.x & 3;
-                const int rows = blockDim.x >> 2;
-                OutT* pdst = out + (int64_t)(threadIdx.x >> 2) * out_stride + q0 + 2 * k;
-                const int64_t pstep = (int64_t)rows * out_stride;
-#pragma unroll 4
-                for (int m = threadIdx.x >> 2; m < N; m += rows, pdst += pstep) {
-                    double2 v2;
-                    v2.x = (double)ws[2 * k].pw[padded(m)];
-                    v2.y = (double)ws[2 * k + 1].pw[padded(m)];
-                    *reinterpret_cast<double2*>(pdst) = v2;
+                for (int m = threadIdx.x / TPR; m < N; m += rows, pdst += pstep) {
+                    if constexpr (VPT == 4) {
+                        float4 v4;
+                        v4.x = dval(4 * k + 0, m);
+                        v4.y = dval(4 * k + 1, m);
+                        v4.z = dval(4 * k + 2, m);
+                        v4.w = dval(4 * k + 3, m);
+                        *reinterpret_cast<float4*>(pdst) = v4;
+                    } else {
+                        double2 v2;
+                        v2.x = (double)dval(2 * k, m);
+                        v2.y = (double)dval(2 * k + 1, m);
+                        *reinterpret_cast<double2*>(pdst) = v2;
+                    }
                 }
             } else {
                 for (int m = threadIdx.x; m < N; m += blockDim.x, dst += step) {
 #pragma unroll
                     for (int j = 0; j < kWarps; ++j)
-                        dst[j] = (OutT)ws[j].pw[padded(m)];
+                        dst[j] = (OutT)dval(j, m);
                 }
             }
         } else {
@@ -361,11 +389,11 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
                 const int li = lag_index ? lag_index[m] : m;
                 if (li < 0) continue;
                 const int64_t dst = dest_of_slot ? dest_of_slot[q0 + j] : q0 + j;
-                out[(int64_t)li * out_stride + dst] = (OutT)ws[j].pw[padded(m)];
+                out[(int64_t)li * out_stride + dst] = (OutT)dval(j, m);
             }
         }
-        // no barrier here: the next sequence's transforms run while the stores drain; pw is
-        // rewritten only after the barrier inside process()
+        // no barrier here: the next sequence's copy wait and mean run while the stores drain;
+        // the exchange buffers are rewritten only after the barrier inside process()
     }
 }
 
@@ -378,12 +406,15 @@ bool temporal_warp_supported(int N, int N2, int scalar_bytes) {
 
 namespace {
 
-// 8 warps (wave vectors) per CTA: 255 registers without spills, one CTA per SM
-constexpr int kTW = 8;
+// Warps (wave vectors) per CTA, one CTA per SM: 12 in map mode (168 registers without
+// spills, the unfold twiddles are not hoisted; 218 KB of shared memory), 8 in ring mode (its
+// per-warp ring accumulators need 4 KB more per warp).
+constexpr int kTW = 12;
+constexpr int kTWRing = 8;
 
 template <typename OutT, bool kDiag, bool kRing>
 cudaError_t launch_w(const TemporalArgs& a, int num_sms, cudaStream_t stream) {
-    constexpr int W = kTW;
+    constexpr int W = kRing ? kTWRing : kTW;
     const size_t smem = sizeof(WarpSmem) * W + 2 * kXS * sizeof(cpx<float>) + kL * sizeof(float) +
                         (kRing ? (size_t)W * kPad * sizeof(float) : 0);
     const int64_t work = kRing ? a.ring.nitems : (a.layout.g_count + W - 1) / W;
