@@ -67,9 +67,15 @@ const void* stage_frames(b200::Engine& eng, const detail::Ingest& in, double& di
     if (in.u8 || (in.source && in.source->contiguous())) {
         const void* src = in.u8 ? static_cast<const void*>(in.u8)
                                 : static_cast<const void*>(in.source->contiguous());
-        b200::check(cudaMemcpyAsync(d, src, ppf * pb * std::size_t(in.frames),
-                                    cudaMemcpyHostToDevice, st), "frame upload");
-        b200::check(cudaStreamSynchronize(st), "sync");
+        const std::size_t bytes = ppf * pb * std::size_t(in.frames);
+        if (detail::is_pinned(src)) {
+            b200::check(cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, st), "frame upload");
+            b200::check(cudaStreamSynchronize(st), "sync");
+        } else {
+            // pageable: the host pool copies through the engine's pinned slots (the driver's
+            // own pageable path is one thread through one bounce buffer, ~10 GB/s)
+            detail::upload_pageable(eng, d, src, bytes, st);
+        }
     } else {
         // FrameSource::read_frame is thread-safe (`frame_source.hpp:16-17`): frames of a
         // 32 MiB chunk are read by a pool of threads into pinned staging, the chunk's DMA to
@@ -92,33 +98,21 @@ const void* stage_frames(b200::Engine& eng, const detail::Ingest& in, double& di
             const int nf = std::min(chunk, in.frames - f0);
             if (used[slot]) b200::check(cudaEventSynchronize(done[slot]), "sync");
             std::uint16_t* buf = pinned[slot];
-            std::atomic<int> next{0};
-            std::exception_ptr failure;
-            std::mutex failure_mu;
-            // raw stacks: each worker takes a contiguous run of frames as one positioned read
+            // raw stacks: each task is a contiguous run of frames read as one positioned read
             const auto* raw = dynamic_cast<const RawStackFileSource*>(in.source);
             static const bool per_frame = std::getenv("DDM_INGEST_PER_FRAME") != nullptr;
             const int run = (raw && !per_frame) ? std::max(1, (nf + nthreads - 1) / nthreads) : 1;
-            auto work = [&] {
-                for (int i = next.fetch_add(run); i < nf; i = next.fetch_add(run)) {
-                    try {
-                        const int cnt = std::min(run, nf - i);
-                        if (raw) raw->read_frames(f0 + i, cnt, buf + std::size_t(i) * ppf);
-                        else in.source->read_frame(f0 + i, {buf + std::size_t(i) * ppf, ppf});
-                    } catch (...) {
-                        std::lock_guard<std::mutex> lk(failure_mu);
-                        if (!failure) failure = std::current_exception();
-                        next = nf;
-                    }
-                }
-            };
-            std::vector<std::thread> pool;
-            for (int t = 1; t < std::min(nthreads, nf); ++t) pool.emplace_back(work);
-            work();
-            for (auto& t : pool) t.join();
-            if (failure) {
+            try {
+                detail::parallel_for(std::size_t((nf + run - 1) / run), [&](std::size_t t) {
+                    const int i = int(t) * run, cnt = std::min(run, nf - i);
+                    if (raw) raw->read_frames(f0 + i, cnt, buf + std::size_t(i) * ppf);
+                    else
+                        for (int k = 0; k < cnt; ++k)
+                            in.source->read_frame(f0 + i + k, {buf + std::size_t(i + k) * ppf, ppf});
+                });
+            } catch (...) {
                 cudaStreamSynchronize(st);
-                std::rethrow_exception(failure);
+                throw;
             }
             b200::check(cudaMemcpyAsync(static_cast<std::uint16_t*>(d) + std::size_t(f0) * ppf, buf,
                                         ppf * 2 * nf, cudaMemcpyHostToDevice, st), "frame upload");
@@ -164,7 +158,9 @@ ResultArchive run_pairwise_core(const Ingest& in, const RunConfig& config,
     b200::Engine& eng = b200::Engine::instance(config.device);
     std::lock_guard<std::mutex> lock(eng.mutex());
     cudaStream_t st = eng.stream();
+    Trace trace("pairwise");
     const void* d_frames = stage_frames(eng, in, timing.disk);
+    trace.lap("stage");
 
     b200::RunSpec spec;
     spec.W = W;
@@ -189,19 +185,20 @@ ResultArchive run_pairwise_core(const Ingest& in, const RunConfig& config,
     spec.out_stride = plane;
     b200::PhaseTimes times;
     eng.run_pairwise(spec, &times);
+    trace.lap("device run");
     bool finite = true;
     double peak = 0.0, lowest = 0.0;
     b200::reduce_stats(d_map, total, st, &finite, &peak, &lowest);
+    trace.lap("stats");
     if (!finite) throw InputError("result map contains non-finite values");
     const double eps = f64 ? 1e-9 : 1e-4;
     if (lowest < -eps * std::max(peak, 1.0))
         throw InputError("result map contains negative values beyond tolerance");
     PhaseClock clock;
     clock.start();
-    b200::check(cudaMemcpyAsync(out, d_map, std::size_t(total) * sizeof(double), cudaMemcpyDeviceToHost, st),
-                "map copy");
-    b200::check(cudaStreamSynchronize(st), "sync");
+    detail::download_pageable(eng, out, d_map, std::size_t(total) * sizeof(double), st);
     clock.stop(timing.merge);
+    trace.lap("map d2h");
     timing.step1 = times.spatial_ms * 1e-3;
     timing.step2 = times.temporal_ms * 1e-3;
     archive.counters.spatial_ffts = direct ? pairs : std::uint64_t(N) * passes;
@@ -370,7 +367,9 @@ ResultArchive run_core(const Ingest& in, const RunConfig& config, double* out,
             b200::check(cudaMemsetAsync(d_map, 0, std::size_t(total) * eb, st), "memset");
         spec.d_out = d_map;
         spec.out_f64 = !widen;
+        trace.lap("prepare");
         eng.run(spec, &times);
+        trace.lap("device run");
         // validate on the device before the copy (`archive.cpp:44-58`)
         bool finite = true;
         double peak = 0.0, lowest = 0.0;
@@ -382,15 +381,15 @@ ResultArchive run_core(const Ingest& in, const RunConfig& config, double* out,
         const double eps = f64 ? 1e-9 : 1e-4;
         if (lowest < -eps * std::max(peak, 1.0))
             throw InputError("result map contains negative values beyond tolerance");
+        trace.lap("stats");
         clock.start();
         if (widen) {
             download_widen(eng, out, static_cast<const float*>(d_map), std::size_t(total), st);
         } else {
-            b200::check(cudaMemcpyAsync(out, d_map, std::size_t(total) * sizeof(double),
-                                        cudaMemcpyDeviceToHost, st), "map copy");
-            b200::check(cudaStreamSynchronize(st), "sync");
+            detail::download_pageable(eng, out, d_map, std::size_t(total) * sizeof(double), st);
         }
         clock.stop(timing.merge);
+        trace.lap("map d2h");
     }
     timing.step1 = times.spatial_ms * 1e-3;
     timing.step2 = times.temporal_ms * 1e-3;
@@ -403,12 +402,16 @@ ResultArchive run_core(const Ingest& in, const RunConfig& config, double* out,
 
 void upload_pageable(b200::Engine& eng, void* dst, const void* src, std::size_t bytes,
                      cudaStream_t stream) {
-    constexpr std::size_t kChunk = std::size_t(32) << 20, kPiece = std::size_t(4) << 20;
-    if (bytes < 2 * kChunk) {
+    // chunks of 1-32 MiB, at least four per copy so the pool's memcpy of one chunk runs
+    // while the previous chunk's DMA is in flight; each chunk is copied in 16 pieces
+    const std::size_t kChunk = std::clamp<std::size_t>(bytes / 4, std::size_t(1) << 20,
+                                                       std::size_t(32) << 20);
+    if (bytes < (std::size_t(1) << 20)) {
         b200::check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream), "upload");
         b200::check(cudaStreamSynchronize(stream), "sync");
         return;
     }
+    const std::size_t kPiece = (kChunk + 15) / 16;
     cudaEvent_t done[2];
     for (auto& e : done) b200::check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     try {
@@ -433,6 +436,59 @@ void upload_pageable(b200::Engine& eng, void* dst, const void* src, std::size_t 
         throw;
     }
     for (auto e : done) cudaEventDestroy(e);
+}
+
+void download_pageable(b200::Engine& eng, void* dst, const void* src, std::size_t bytes,
+                       cudaStream_t stream) {
+    if (bytes < (std::size_t(1) << 20) || is_pinned(dst)) {
+        b200::check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, stream), "download");
+        b200::check(cudaStreamSynchronize(stream), "sync");
+        return;
+    }
+    // DMA of chunk i+1 into one pinned slot while the pool copies chunk i out of the other
+    const std::size_t kChunk = std::clamp<std::size_t>(bytes / 4, std::size_t(1) << 20,
+                                                       std::size_t(32) << 20);
+    const std::size_t kPiece = (kChunk + 15) / 16;
+    const std::size_t chunks = (bytes + kChunk - 1) / kChunk;
+    cudaEvent_t done[2];
+    for (auto& e : done) b200::check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    char* pin[2] = {static_cast<char*>(eng.pinned(0, kChunk)), static_cast<char*>(eng.pinned(1, kChunk))};
+    const char* s = static_cast<const char*>(src);
+    char* d = static_cast<char*>(dst);
+    auto issue = [&](std::size_t i) {
+        const std::size_t off = i * kChunk, n = std::min(kChunk, bytes - off);
+        b200::check(cudaMemcpyAsync(pin[i & 1], s + off, n, cudaMemcpyDeviceToHost, stream), "download");
+        b200::check(cudaEventRecord(done[i & 1], stream), "event");
+    };
+    try {
+        issue(0);
+        for (std::size_t i = 0; i < chunks; ++i) {
+            if (i + 1 < chunks) issue(i + 1);
+            b200::check(cudaEventSynchronize(done[i & 1]), "event sync");
+            const std::size_t off = i * kChunk, n = std::min(kChunk, bytes - off);
+            const char* p = pin[i & 1];
+            parallel_for((n + kPiece - 1) / kPiece, [&](std::size_t k) {
+                const std::size_t o = k * kPiece;
+                std::memcpy(d + off + o, p + o, std::min(kPiece, n - o));
+            });
+            // slot i & 1 is reused by chunk i + 2, issued after this copy-out
+        }
+        b200::check(cudaStreamSynchronize(stream), "sync");
+    } catch (...) {
+        cudaStreamSynchronize(stream);
+        for (auto e : done) cudaEventDestroy(e);
+        throw;
+    }
+    for (auto e : done) cudaEventDestroy(e);
+}
+
+bool is_pinned(const void* p) {
+    cudaPointerAttributes attr{};
+    if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return attr.type == cudaMemoryTypeHost;
 }
 
 void download_widen(b200::Engine& eng, double* out, const float* d, std::size_t n, cudaStream_t stream) {

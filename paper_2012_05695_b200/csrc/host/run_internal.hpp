@@ -18,6 +18,7 @@
 #include <new>
 #include <string>
 #include <thread>
+#include <type_traits>
 #include <vector>
 
 namespace ddm::detail {
@@ -40,30 +41,16 @@ std::filesystem::path write_partial_payload(const PartialResult& header, const d
 ResultArchive run_core(const Ingest& in, const RunConfig& config, double* out,
                        std::int64_t capacity);
 
-// fn(i) for i in [0, n) on up to 16 host threads; the first exception is rethrown
+// fn(i) for i in [0, n) on up to 16 host threads of a persistent pool (pool.cpp: workers are
+// created once per process, so a call costs a wake-up, not thread creation); the first
+// exception is rethrown. Calls from inside a pool task run inline.
+void parallel_for_impl(std::size_t n, void (*call)(void*, std::size_t), void* ctx);
+
 template <class Fn>
 void parallel_for(std::size_t n, Fn&& fn) {
-    const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
-    const std::size_t nt = std::min<std::size_t>(n, hw);
-    std::atomic<std::size_t> next{0};
-    std::exception_ptr err;
-    std::mutex mu;
-    auto work = [&] {
-        for (std::size_t i; (i = next.fetch_add(1)) < n;) {
-            try {
-                fn(i);
-            } catch (...) {
-                std::lock_guard<std::mutex> lock(mu);
-                if (!err) err = std::current_exception();
-                next.store(n);
-            }
-        }
-    };
-    std::vector<std::thread> pool;
-    for (std::size_t t = 1; t < nt; ++t) pool.emplace_back(work);
-    work();
-    for (auto& t : pool) t.join();
-    if (err) std::rethrow_exception(err);
+    using F = std::remove_reference_t<Fn>;
+    parallel_for_impl(n, [](void* c, std::size_t i) { (*static_cast<F*>(c))(i); },
+                      const_cast<void*>(static_cast<const void*>(&fn)));
 }
 
 // Host -> device copy of a large pageable buffer through the engine's two pinned slots:
@@ -72,6 +59,12 @@ void parallel_for(std::size_t n, Fn&& fn) {
 // the engine lock; the copy is complete on `stream` when this returns.
 void upload_pageable(b200::Engine& eng, void* dst, const void* src, std::size_t bytes,
                      cudaStream_t stream);
+// Device -> host copy into pageable memory through the two pinned slots (pinned or small
+// destinations: one cudaMemcpy); complete when this returns
+void download_pageable(b200::Engine& eng, void* dst, const void* src, std::size_t bytes,
+                       cudaStream_t stream);
+// page-locked (cudaMallocHost / registered) host memory: DMA reads it directly
+bool is_pinned(const void* p);
 
 // Device f32 -> host f64 (exact widening): chunks of the f32 map stream through the engine's
 // two pinned slots while host threads widen the previous chunk into `out`, so PCIe carries

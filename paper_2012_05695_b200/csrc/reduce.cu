@@ -6,6 +6,8 @@
 //                   (lag, bin) sum is reduced by one warp in a fixed order).
 #include <cfloat>
 #include <cmath>
+#include <map>
+#include <mutex>
 
 #include "engine.hpp"
 
@@ -83,16 +85,30 @@ __global__ void ring_sums_kernel(const T* __restrict__ values, int64_t n_lags, i
 template <typename T>
 static void reduce_stats_t(const T* d, int64_t n, cudaStream_t stream, bool* finite, double* max_v,
                            double* min_v) {
-    const int blocks = 296, threads = 256;
-    double* part = nullptr;
-    check(cudaMallocAsync(reinterpret_cast<void**>(&part), sizeof(double) * 3 * blocks, stream),
-          "cudaMallocAsync");
-    stats_kernel<T><<<blocks, threads, 0, stream>>>(d, n, part);
+    constexpr int blocks = 296, threads = 256;
+    // per-device partials and their pinned host copy, allocated once: a cudaMallocAsync /
+    // pageable copy per call cost ~0.4 ms next to sub-millisecond runs
+    struct Slot {
+        double* dev = nullptr;
+        double* host = nullptr;
+    };
+    static std::mutex mu;
+    static std::map<int, Slot> slots;
+    int device = 0;
+    check(cudaGetDevice(&device), "cudaGetDevice");
+    std::lock_guard<std::mutex> lock(mu);
+    Slot& sl = slots[device];
+    if (!sl.dev) {
+        check(cudaMalloc(reinterpret_cast<void**>(&sl.dev), sizeof(double) * 3 * blocks), "cudaMalloc");
+        check(cudaMallocHost(reinterpret_cast<void**>(&sl.host), sizeof(double) * 3 * blocks),
+              "cudaMallocHost");
+    }
+    stats_kernel<T><<<blocks, threads, 0, stream>>>(d, n, sl.dev);
     check(cudaGetLastError(), "stats kernel");
-    double host[3 * 296];
-    check(cudaMemcpyAsync(host, part, sizeof(host), cudaMemcpyDeviceToHost, stream), "stats copy");
-    check(cudaFreeAsync(part, stream), "cudaFreeAsync");
+    check(cudaMemcpyAsync(sl.host, sl.dev, sizeof(double) * 3 * blocks, cudaMemcpyDeviceToHost, stream),
+          "stats copy");
     check(cudaStreamSynchronize(stream), "sync");
+    const double* host = sl.host;
     double mx = -DBL_MAX, mn = DBL_MAX, bad = 0.0;
     for (int i = 0; i < blocks; ++i) {
         mx = std::fmax(mx, host[3 * i]);
