@@ -10,9 +10,20 @@
 //   u(k)    = |X(2k)|^2 + i |X(2k+1)|^2                          (P = |X|^2 in f32, `:60-64`)
 //   U       = IFFT_L(u);  corr(m) = Re[E(m) + W_N2^{-m} O(m)] / N2  (real-input unfold, `:65-73`)
 //   d(m)    = (S(m) - 2 corr(m)) / (N - m), d(0) = 0             (`:114-129`, `scheduler.cpp:157`)
-// The time mean only conditions the subtraction (d is offset invariant, `temporal.hpp:258-262`),
-// so it is formed with a pairwise f32 sum; everything the reference keeps in f64 (power,
-// averages term, combination) stays f64.
+// Working precision: the FFTs, P = |X|^2 and |t|^2 are f32 as in the reference's f32
+// engine (`temporal.cpp:56-64` computes in S); the mean is a pairwise f32 sum (it only
+// conditions the subtraction: d is offset invariant, `temporal.hpp:258-262`); S(m) is summed
+// in f32 within each lane's run of 32 terms with the 32 lane totals carried in f64; the
+// combination is one f32 FMA. The reference keeps power, d_a and the combination in f64
+// (`temporal.cpp:24-41,114-129`); here their f32 rounding (~1e-7 relative) stays below the
+// f32 transform error both engines share, measured at every BASELINE shape against the
+// reference's own f32 maps (relative L2 1.5e-6 at C2, tests/test_gpu_shapes.py up to C4).
+//
+// Why one CTA-wide barrier per tile (all 12 warps in phase): splitting the CTA into three
+// 4-warp groups on named barriers (measured, r02i) cost 7%: the groups' 16-byte row pieces
+// were written at different times, so L2 evicted half-written sectors (ECC read-modify-write:
+// +376 MB DRAM reads, +318 MB writes per launch), and warps running different parts of the
+// 117 KB unrolled kernel raised instruction-fetch stalls from 0.17 to 0.46 per issue.
 //
 // Data movement per sequence: one TMA bulk copy (cp.async.bulk, 8 KB) into the warp's stage,
 // which stays resident through all three transforms (the odd transform re-reads it, the
@@ -80,7 +91,6 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     WarpSmem& my = ws[warp];
-    float* scf = reinterpret_cast<float*>(my.scratch);
 
     for (int m = threadIdx.x; m < N; m += blockDim.x) rcp[m] = (float)(1.0 / (double)(N - m));
     if (lane == 0) {
