@@ -190,6 +190,65 @@ void Engine::check_stream_flag() {
         throw CudaError("streamed spatial pass: a column CTA gave up waiting for the row pass");
 }
 
+void Engine::wait_frames(cudaStream_t st, int frame_end) {
+    if (!frames_ready_) return;
+    for (const auto& fr : *frames_ready_)
+        if (fr.first >= frame_end) {
+            check(cudaStreamWaitEvent(st, fr.second, 0), "wait for frames");
+            return;
+        }
+    if (!frames_ready_->empty()) check(cudaStreamWaitEvent(st, frames_ready_->back().second, 0), "wait for frames");
+}
+
+std::vector<std::pair<int, cudaEvent_t>> Engine::upload_frames_async(void* d_frames, const void* host, int N,
+                                                                      size_t frame_bytes, int chunks) {
+    check(cudaSetDevice(device_), "cudaSetDevice");
+    if (!h2d_stream_) check(cudaStreamCreateWithFlags(&h2d_stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+    chunks = std::max(1, std::min(chunks, N));
+    while (h2d_events_.size() < (size_t)chunks + 2) {
+        cudaEvent_t e = nullptr;
+        check(cudaEventCreate(&e), "cudaEventCreate");
+        h2d_events_.push_back(e);
+    }
+    h2d_chunks_ = chunks;
+    // the upload must not overtake work already queued on the engine stream that reads the
+    // previous frames
+    check(cudaEventRecord(h2d_events_[chunks], stream_), "cudaEventRecord");
+    check(cudaStreamWaitEvent(h2d_stream_, h2d_events_[chunks], 0), "stream wait");
+    check(cudaEventRecord(h2d_events_[chunks + 1], h2d_stream_), "cudaEventRecord");
+    std::vector<std::pair<int, cudaEvent_t>> ready;
+    for (int c = 0; c < chunks; ++c) {
+        const int f0 = (int)((int64_t)N * c / chunks), f1 = (int)((int64_t)N * (c + 1) / chunks);
+        check(cudaMemcpyAsync(static_cast<char*>(d_frames) + (size_t)f0 * frame_bytes,
+                              static_cast<const char*>(host) + (size_t)f0 * frame_bytes,
+                              (size_t)(f1 - f0) * frame_bytes, cudaMemcpyHostToDevice, h2d_stream_),
+              "frame upload");
+        check(cudaEventRecord(h2d_events_[c], h2d_stream_), "cudaEventRecord");
+        ready.emplace_back(f1, h2d_events_[c]);
+    }
+    return ready;
+}
+
+double Engine::upload_ms() {
+    if (h2d_chunks_ == 0) return 0.0;
+    check(cudaEventSynchronize(h2d_events_[h2d_chunks_ - 1]), "upload");
+    float ms = 0.f;
+    check(cudaEventElapsedTime(&ms, h2d_events_[h2d_chunks_ + 1], h2d_events_[h2d_chunks_ - 1]), "event time");
+    return ms;
+}
+
+bool Engine::finish_host_out(PhaseTimes* times) {
+    if (!d2h_pending_) return false;
+    d2h_pending_ = false;
+    check(cudaStreamSynchronize(d2h_stream_), "map copy");
+    if (times) {
+        float ms = 0.f;
+        check(cudaEventElapsedTime(&ms, d2h_events_[0], d2h_events_[1]), "event time");
+        times->d2h_ms += ms;
+    }
+    return true;
+}
+
 Engine::~Engine() {
     cudaSetDevice(device_);
     if (stream_flag_) cudaFreeHost(stream_flag_);
@@ -198,6 +257,10 @@ Engine::~Engine() {
     for (auto e : timing_events_) cudaEventDestroy(e);
     for (auto e : chunk_events_) cudaEventDestroy(e);
     if (cols_stream_) cudaStreamDestroy(cols_stream_);
+    if (d2h_stream_) cudaStreamDestroy(d2h_stream_);
+    if (h2d_stream_) cudaStreamDestroy(h2d_stream_);
+    for (auto e : h2d_events_) cudaEventDestroy(e);
+    for (auto e : d2h_events_) cudaEventDestroy(e);
     for (auto& e : ev_)
         if (e) cudaEventDestroy(e);
     if (stream_) cudaStreamDestroy(stream_);
@@ -332,6 +395,7 @@ void Engine::spatial_pass(ddmk::SpatialArgs sa, bool f64, bool warp_s, PhaseTime
         const int ahead = env_ahead > 0 ? env_ahead : 3;
         check(cudaEventRecord(chunk_events_[0], stream_), "cudaEventRecord");
         check(cudaStreamWaitEvent(cols_stream_, chunk_events_[0], 0), "stream wait");
+        wait_frames(stream_, N);
         check(ddmk::launch_spatial_warp_stream(sa, ctl, ahead, rows_per_sm * num_sms_, cols_per_sm * num_sms_,
                                                stream_, cols_stream_), "streamed spatial pass");
         check(cudaEventRecord(chunk_events_[1], cols_stream_), "cudaEventRecord");
@@ -366,6 +430,7 @@ void Engine::spatial_pass(ddmk::SpatialArgs sa, bool f64, bool warp_s, PhaseTime
             sa.mid = static_cast<char*>(d_mid) + (size_t)(k & 1) * F * per_frame;
             // the buffer is free once the column pass of chunk k-2 has read it
             if (k >= 2) check(cudaStreamWaitEvent(stream_, chunk_events_[2 * (k - 2) + 1], 0), "wait");
+            wait_frames(stream_, sa.frame0 + sa.nframes);
             check(ddmk::launch_spatial_warp<float>(sa, stream_, 1), "row pass");
             check(cudaEventRecord(rows_done, stream_), "cudaEventRecord");
             check(cudaStreamWaitEvent(cols_stream_, rows_done, 0), "wait");
@@ -378,6 +443,7 @@ void Engine::spatial_pass(ddmk::SpatialArgs sa, bool f64, bool warp_s, PhaseTime
         for (int f0 = 0; f0 < N; f0 += F) {
             sa.frame0 = f0;
             sa.nframes = std::min(F, N - f0);
+            wait_frames(stream_, f0 + sa.nframes);
             check(warp_s ? ddmk::launch_spatial_warp<float>(sa, stream_)
                   : f64 ? ddmk::launch_spatial<double>(sa, stream_)
                         : ddmk::launch_spatial<float>(sa, stream_), "spatial kernels");
@@ -404,6 +470,7 @@ const int* Engine::upload_lags(const std::vector<int64_t>& lags, int N) {
 
 uint64_t Engine::run(const RunSpec& sp, PhaseTimes* times) {
     check(cudaSetDevice(device_), "cudaSetDevice");
+    finish_host_out(nullptr);   // copies of an earlier call that never drained them
     const int W = sp.W, H = sp.H, N = sp.N;
     const int Wh = W / 2 + 1;
     const int64_t plane = (int64_t)H * Wh;
@@ -468,6 +535,17 @@ uint64_t Engine::run(const RunSpec& sp, PhaseTimes* times) {
     };
 
     last_engines_ = describe(warp_s, W, H, warp_t, long_t, N2, T, gmax, N, false);
+    // end-to-end streaming (RunSpec::frames_ready / host_out)
+    frames_ready_ = sp.frames_ready.empty() ? nullptr : &sp.frames_ready;
+    struct ResetFrames {
+        const std::vector<std::pair<int, cudaEvent_t>>*& p;
+        ~ResetFrames() { p = nullptr; }
+    } reset_frames{frames_ready_};
+    static const int kOutChunks = std::getenv("DDM_OUT_CHUNKS") ? std::atoi(std::getenv("DDM_OUT_CHUNKS")) : 8;
+    const bool stream_out = kOutChunks > 0 && sp.host_out && warp_t && !sp.partial_mode && sp.identity &&
+                            sp.groups.size() == 1 && sp.d_out;
+    if (stream_out && !d2h_stream_)
+        check(cudaStreamCreateWithFlags(&d2h_stream_, cudaStreamNonBlocking), "cudaStreamCreate");
     uint64_t spatial_passes = 0;
     for (size_t gi = 0; gi < sp.groups.size(); ++gi) {
         const int64_t gb = sp.groups[gi].first, gc = sp.groups[gi].second - gb;
@@ -512,6 +590,37 @@ uint64_t Engine::run(const RunSpec& sp, PhaseTimes* times) {
             check(ddmk::launch_temporal_long(ta, num_sms_, out_q, stream_), "temporal kernel");
             if (times) times->temporal_launches += 2 * (int)((gc + ddmk::temporal_long_chunk(N) - 1) /
                                                              ddmk::temporal_long_chunk(N));
+        } else if (stream_out) {
+            // wave-vector chunks: chunk c's columns of every lag row go to the host on the
+            // D2H stream while chunk c + 1 computes (2D copies, one row segment per lag)
+            const int chunks = (int)std::min<int64_t>(kOutChunks, std::max<int64_t>(1, gc / 4096));
+            while (d2h_events_.size() < (size_t)(chunks + 2)) {
+                cudaEvent_t e = nullptr;
+                check(cudaEventCreate(&e), "cudaEventCreate");
+                d2h_events_.push_back(e);
+            }
+            for (int c = 0; c < chunks; ++c) {
+                // 12-aligned chunk edges keep the kernel's full-tile vector stores
+                const int64_t qa = (gc * c / chunks) / 12 * 12;
+                const int64_t qb = c + 1 == chunks ? gc : (gc * (c + 1) / chunks) / 12 * 12;
+                ddmk::TemporalArgs tc = ta;
+                tc.spec = static_cast<const char*>(d_spec) + (size_t)qa * N * cs;
+                tc.layout.g_begin = gb + qa;
+                tc.layout.g_count = qb - qa;
+                tc.out = static_cast<char*>(ta.out) + (size_t)qa * ob;
+                check(ddmk::launch_temporal_warp(tc, num_sms_, stream_), "temporal kernel");
+                check(cudaEventRecord(d2h_events_[c + 2], stream_), "cudaEventRecord");
+                check(cudaStreamWaitEvent(d2h_stream_, d2h_events_[c + 2], 0), "stream wait");
+                if (c == 0) check(cudaEventRecord(d2h_events_[0], d2h_stream_), "cudaEventRecord");
+                const size_t pitch = (size_t)ta.out_stride * ob;
+                check(cudaMemcpy2DAsync(static_cast<char*>(sp.host_out) + (size_t)(gb + qa) * ob, pitch,
+                                        tc.out, pitch, (size_t)(qb - qa) * ob, sp.lags.size(),
+                                        cudaMemcpyDeviceToHost, d2h_stream_),
+                      "map chunk copy");
+            }
+            check(cudaEventRecord(d2h_events_[1], d2h_stream_), "cudaEventRecord");
+            d2h_pending_ = true;
+            if (times) times->temporal_launches += chunks;
         } else {
             check(warp_t ? ddmk::launch_temporal_warp(ta, num_sms_, stream_)
                          : sp.f64 ? ddmk::launch_temporal<double>(ta, stream_)

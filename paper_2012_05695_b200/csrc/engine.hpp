@@ -50,6 +50,7 @@ struct PhaseTimes {
     double temporal_ms = 0.0;
     int spatial_launches = 0;
     int temporal_launches = 0;
+    double d2h_ms = 0.0;      // host_out mode: first map chunk copy start -> last copy end
 };
 
 struct RunSpec {
@@ -69,6 +70,15 @@ struct RunSpec {
     int64_t out_stride = 0;
     bool partial_mode = false;
     std::function<void(size_t group, const void* d_partial, int64_t g_count)> on_partial;
+    // End-to-end streaming (optional):
+    //   frames_ready: (frames resident, event) pairs in ascending frame order, recorded on the
+    //   caller's upload stream; the spatial pass waits for the event covering each chunk.
+    //   host_out: page-locked host map (same layout as d_out): the temporal pass runs in
+    //   wave-vector chunks and each chunk's columns of every lag row are copied out on the
+    //   engine's D2H stream while the next chunk computes (single-group identity map, warp
+    //   temporal engine); the copies complete by finish_host_out().
+    std::vector<std::pair<int, cudaEvent_t>> frames_ready;
+    void* host_out = nullptr;
 };
 
 // Ring geometry of a retained wave-vector set for the azimuthal average
@@ -100,6 +110,18 @@ public:
     // Runs every group of `spec` on the engine stream (asynchronous w.r.t. the host unless
     // on_partial needs the data). Returns the number of spatial passes (= frames x groups).
     uint64_t run(const RunSpec& spec, PhaseTimes* times = nullptr);
+
+    // Pinned host frames -> frame buffer in `chunks` pieces on the engine's upload stream;
+    // returns (frames resident, event) pairs for RunSpec::frames_ready (valid until the next
+    // call). The copies are ordered after nothing else; the caller holds the engine lock.
+    std::vector<std::pair<int, cudaEvent_t>> upload_frames_async(void* d_frames, const void* host,
+                                                                  int N, size_t frame_bytes, int chunks);
+
+    // Waits for the map copies a host_out run() queued (no-op otherwise); adds their span to
+    // times->d2h_ms. Returns whether run() streamed the map out.
+    bool finish_host_out(PhaseTimes* times);
+    // duration of the last upload_frames_async (waits for it)
+    double upload_ms();
 
     // Batched SequenceEngine::with_ft: q sequences of n complex values, q-major on device
     // (working precision). d_out [q][n] f64; optional d_a / corr [q][n] f64 restored to the
@@ -187,6 +209,15 @@ private:
     std::vector<cudaEvent_t> timing_events_;   // reusable phase-timing events
     std::vector<cudaEvent_t> chunk_events_;    // row/column pass ordering across streams
     cudaStream_t cols_stream_ = nullptr;       // column passes (overlapped spatial step)
+    cudaStream_t d2h_stream_ = nullptr;        // map chunks out (RunSpec::host_out)
+    bool d2h_pending_ = false;
+    cudaStream_t h2d_stream_ = nullptr;        // frame chunks in (upload_frames_async)
+    std::vector<cudaEvent_t> h2d_events_;      // per frame chunk, [chunks] order, [chunks+1] start
+    int h2d_chunks_ = 0;
+    std::vector<cudaEvent_t> d2h_events_;      // [0] first copy start, [1] last copy end, [2..] chunks
+    // spatial passes: wait on stream `st` until frames [0, frame_end) are resident
+    const std::vector<std::pair<int, cudaEvent_t>>* frames_ready_ = nullptr;
+    void wait_frames(cudaStream_t st, int frame_end);
     void* pinned_[2] = {nullptr, nullptr};
     size_t pinned_bytes_[2] = {0, 0};
     // streamed spatial pass: its give-up flag lands in pinned memory; checked after the next

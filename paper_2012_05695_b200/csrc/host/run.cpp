@@ -58,7 +58,11 @@ fs::path make_temp_dir() {
 
 // Frames -> device buffer of the engine. A contiguous u16/u8 source is one copy; otherwise
 // frames are read through the FrameSource interface into pinned staging, double buffered.
-const void* stage_frames(b200::Engine& eng, const detail::Ingest& in, double& disk_s) {
+// ready != nullptr: a page-locked contiguous stack is uploaded asynchronously in chunks
+// (Engine::upload_frames_async) and *ready receives the per-chunk events for
+// RunSpec::frames_ready; disk_s is then left to the caller (Engine::upload_ms).
+const void* stage_frames(b200::Engine& eng, const detail::Ingest& in, double& disk_s,
+                         std::vector<std::pair<int, cudaEvent_t>>* ready = nullptr) {
     const auto t0 = std::chrono::steady_clock::now();
     const std::size_t ppf = std::size_t(in.width) * in.height;
     const std::size_t pb = in.u8 ? 1 : 2;
@@ -68,6 +72,11 @@ const void* stage_frames(b200::Engine& eng, const detail::Ingest& in, double& di
         const void* src = in.u8 ? static_cast<const void*>(in.u8)
                                 : static_cast<const void*>(in.source->contiguous());
         const std::size_t bytes = ppf * pb * std::size_t(in.frames);
+        if (ready && detail::is_pinned(src) && bytes >= (std::size_t(8) << 20)) {
+            // four chunks: the first spatial chunk starts once its half of the stack is in
+            *ready = eng.upload_frames_async(d, src, in.frames, ppf * pb, 4);
+            return d;
+        }
         if (detail::is_pinned(src)) {
             b200::check(cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, st), "frame upload");
             b200::check(cudaStreamSynchronize(st), "sync");
@@ -259,7 +268,9 @@ ResultArchive run_core(const Ingest& in, const RunConfig& config, double* out,
     cudaStream_t st = eng.stream();
 
     Trace trace("run");
-    const void* d_frames = stage_frames(eng, in, timing.disk);
+    const bool keep_partials_early = !config.out_dir.empty() || bool(config.before_merge);
+    std::vector<std::pair<int, cudaEvent_t>> frames_ready;
+    const void* d_frames = stage_frames(eng, in, timing.disk, keep_partials_early ? nullptr : &frames_ready);
     trace.lap("stage");
 
     b200::RunSpec spec;
@@ -367,28 +378,49 @@ ResultArchive run_core(const Ingest& in, const RunConfig& config, double* out,
             b200::check(cudaMemsetAsync(d_map, 0, std::size_t(total) * eb, st), "memset");
         spec.d_out = d_map;
         spec.out_f64 = !widen;
+        spec.frames_ready = frames_ready;
+        // a page-locked destination: the map streams out chunk by chunk while the temporal
+        // pass runs (Engine::run, RunSpec::host_out)
+        if (!widen && detail::is_pinned(out)) spec.host_out = out;
         trace.lap("prepare");
+        // map copies still in flight into `out` are drained on every exit path
+        struct DrainCopies {
+            b200::Engine& e;
+            ~DrainCopies() {
+                try {
+                    e.finish_host_out(nullptr);
+                } catch (...) {
+                }
+            }
+        } drain_copies{eng};
         eng.run(spec, &times);
+        if (!frames_ready.empty()) timing.disk += eng.upload_ms() * 1e-3;
         trace.lap("device run");
-        // validate on the device before the copy (`archive.cpp:44-58`)
+        // validate on the device (`archive.cpp:44-58`): before the copy, or beside the map
+        // chunks still streaming out (their copies are drained before any error is thrown)
         bool finite = true;
         double peak = 0.0, lowest = 0.0;
         if (widen)
             b200::reduce_stats(static_cast<const float*>(d_map), total, st, &finite, &peak, &lowest);
         else
             b200::reduce_stats(static_cast<const double*>(d_map), total, st, &finite, &peak, &lowest);
+        trace.lap("stats");
+        const bool streamed = eng.finish_host_out(&times);
         if (!finite) throw InputError("result map contains non-finite values");
         const double eps = f64 ? 1e-9 : 1e-4;
         if (lowest < -eps * std::max(peak, 1.0))
             throw InputError("result map contains negative values beyond tolerance");
-        trace.lap("stats");
-        clock.start();
-        if (widen) {
-            download_widen(eng, out, static_cast<const float*>(d_map), std::size_t(total), st);
+        if (streamed) {
+            // the copies overlapped the temporal pass; merge = their span
+            timing.merge += times.d2h_ms * 1e-3;
         } else {
-            detail::download_pageable(eng, out, d_map, std::size_t(total) * sizeof(double), st);
+            clock.start();
+            if (widen)
+                download_widen(eng, out, static_cast<const float*>(d_map), std::size_t(total), st);
+            else
+                detail::download_pageable(eng, out, d_map, std::size_t(total) * sizeof(double), st);
+            clock.stop(timing.merge);
         }
-        clock.stop(timing.merge);
         trace.lap("map d2h");
     }
     timing.step1 = times.spatial_ms * 1e-3;
