@@ -25,12 +25,12 @@
 // +376 MB DRAM reads, +318 MB writes per launch), and warps running different parts of the
 // 117 KB unrolled kernel raised instruction-fetch stalls from 0.17 to 0.46 per issue.
 //
-// Data movement per sequence: one TMA bulk copy (cp.async.bulk, 8 KB) into the warp's stage,
-// which stays resident through all three transforms (the odd transform re-reads it, the
-// averages term reads |t|^2 from it after the inverse); the next sequence's copy is issued
-// right after that, so it lands during the unfold and the tile store (an L2 prefetch of the
-// same bytes goes out one sequence earlier). Three four-step FFTs (warp_fft.cuh, one
-// shared-memory exchange each); the exchange buffer then holds |t|^2, S(m) and d(m); the
+// Data movement per sequence: one TMA bulk copy (cp.async.bulk, 8 KB) into the warp's stage.
+// The first pass writes the shifted sequence back; the odd transform re-reads it and leaves
+// |t|^2 in its place for the averages term; once that has been read the next sequence's copy
+// is issued, so it lands during the S(m) scan, the unfold and the tile store (an L2 prefetch
+// of the same bytes goes out one sequence earlier). Three four-step FFTs (warp_fft.cuh, one
+// shared-memory exchange each); the exchange buffer then holds S(m) and d(m); the
 // unfold reads U(L-m) from the mirrored lane with shuffles; a CTA of 12 warps stores 12
 // consecutive wave vectors per lag row.
 //
@@ -186,11 +186,13 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
             mx *= inv_nf;
             my_ *= inv_nf;
         }
+        // shift once and write t back: the odd transform re-reads the shifted sequence
 #pragma unroll
         for (int b = 0; b < 32; ++b) {
             if (lane + 32 * b < N) {
                 v[b].x -= mx;
                 v[b].y -= my_;
+                my.stage[lane + 32 * b] = v[b];
             }
         }
 
@@ -205,38 +207,23 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
 #pragma unroll
         for (int d = 0; d < 32; ++d) pe[d] = v[d].x * v[d].x + v[d].y * v[d].y;
 
-        // ---- odd outputs: t again from the stage
+        // ---- odd outputs: t again from the stage; its last read, so |t|^2 (f32, of the
+        //      shifted sequence) replaces it there for the averages term
 #pragma unroll
         for (int b = 0; b < 32; ++b) {
             const int n = lane + 32 * b;
-            cpx<float> x = (live && n < N) ? my.stage[n] : cpx<float>{0.f, 0.f};
-            if (n < N) {
-                x.x -= mx;
-                x.y -= my_;
-            }
-            v[b] = x;
+            v[b] = (n < N) ? my.stage[n] : cpx<float>{0.f, 0.f};
         }
+        __syncwarp();
+        float* pw = reinterpret_cast<float*>(my.stage);   // |t|^2 at padded(n)
+#pragma unroll
+        for (int b = 0; b < 32; ++b) pw[padded(lane + 32 * b)] = v[b].x * v[b].x + v[b].y * v[b].y;
         fft1024<-1, true>(v, my.scratch, lane, tw_odd);
 #pragma unroll
         for (int d = 0; d < 32; ++d) v[d] = {pe[d], v[d].x * v[d].x + v[d].y * v[d].y};
 
         // ---- half-length inverse: lane c holds U[c + 32 d] in v[d]
         fft1024<+1, false>(v, my.scratch, lane, tw_even);
-
-        // ---- |t|^2 (f32, of the shifted sequence) from the stage into the now free exchange
-        //      buffer; then the stage is free: start the next sequence's copy
-#pragma unroll
-        for (int b = 0; b < 32; ++b) {
-            const int n = lane + 32 * b;
-            cpx<float> x = (live && n < N) ? my.stage[n] : cpx<float>{0.f, 0.f};
-            if (n < N) {
-                x.x -= mx;
-                x.y -= my_;
-            }
-            sw[padded(n)] = x.x * x.x + x.y * x.y;
-        }
-        __syncwarp();
-        after_stage();
 
         // ---- S(m) = sum_{n >= m} (p_n + p_{N-1-n}) = (N - m) d_a(m)  (`temporal.cpp:19-42`):
         //      lane a scans n = 32 a + j in f32, lane totals are suffix-summed in f64
@@ -246,8 +233,11 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
                 const int n = 32 * lane + j;
-                qv[j] = (n < N) ? sw[padded(n)] + sw[padded(N - 1 - n)] : 0.f;
+                qv[j] = (n < N) ? pw[padded(n)] + pw[padded(N - 1 - n)] : 0.f;
             }
+            // the stage has been read for the last time: start the next sequence's copy
+            __syncwarp();
+            after_stage();
             float r = 0.f;
 #pragma unroll
             for (int j = 31; j >= 0; --j) {
