@@ -178,18 +178,6 @@ void* Engine::pinned(int slot, size_t bytes) {
     return pinned_[slot];
 }
 
-unsigned* Engine::stream_flag_host() {
-    if (!stream_flag_) check(cudaMallocHost(&stream_flag_, sizeof(unsigned)), "cudaMallocHost");
-    return stream_flag_;
-}
-
-void Engine::check_stream_flag() {
-    if (!stream_flag_pending_) return;
-    stream_flag_pending_ = false;
-    if (*stream_flag_ != 0u)
-        throw CudaError("streamed spatial pass: a column CTA gave up waiting for the row pass");
-}
-
 void Engine::wait_frames(cudaStream_t st, int frame_end) {
     if (!frames_ready_) return;
     for (const auto& fr : *frames_ready_)
@@ -251,7 +239,6 @@ bool Engine::finish_host_out(PhaseTimes* times) {
 
 Engine::~Engine() {
     cudaSetDevice(device_);
-    if (stream_flag_) cudaFreeHost(stream_flag_);
     for (auto p : pinned_)
         if (p) cudaFreeHost(p);
     for (auto e : timing_events_) cudaEventDestroy(e);
@@ -354,58 +341,6 @@ void Engine::spatial_pass(ddmk::SpatialArgs sa, bool f64, bool warp_s, PhaseTime
         F = std::min(N, std::max(Fc, F - F % Fc));
     }
     last_F_ = F;
-    // Streamed pass (opt-in, DDM_SPATIAL_STREAM=1): persistent row and column kernels side by
-    // side, the column pass reading each chunk's `mid` from L2 right after it is written
-    // (spatial_warp.cu). `mid` spans the whole stack, so the pass never depends on both
-    // kernels being resident at once. Measured at C2 (r02j): 0.85 ms against 0.77 ms for the
-    // two-chunk pass: sharing each SM between the two kernels leaves the row pass 16 warps
-    // and the column pass 8, and both are issue-bound once `mid` no longer goes to DRAM
-    // (437 M warp instructions per step at 44% issue efficiency).
-    static const char* stream_env = std::getenv("DDM_SPATIAL_STREAM");
-    const int Fc = warp_s ? ddmk::spatial_warp_col_frames(sa.H) : 0;
-    const bool stream = warp_s && sa.peers.ranks == 0 && N >= 2 * Fc &&
-                        (size_t)Fc * per_frame <= (size_t(40) << 20) &&
-                        (stream_env && stream_env[0] == '1');
-    if (stream) {
-        last_F_ = Fc;
-        sa.frame0 = 0;
-        sa.nframes = N;
-        sa.mid = mid_.ensure((size_t)N * per_frame);
-        const int words = ddmk::spatial_stream_ctl_words(N, sa.H);
-        unsigned* ctl = static_cast<unsigned*>(buffer("spatial_stream_ctl", (size_t)words * sizeof(unsigned)));
-        check(cudaMemsetAsync(ctl, 0, (size_t)words * sizeof(unsigned), stream_), "memset");
-        if (!cols_stream_)
-            check(cudaStreamCreateWithFlags(&cols_stream_, cudaStreamNonBlocking), "cudaStreamCreate");
-        if (chunk_events_.size() < 2) {
-            while (chunk_events_.size() < 2) {
-                cudaEvent_t e = nullptr;
-                check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
-                chunk_events_.push_back(e);
-            }
-        }
-        int rps = 0, cps = 0;
-        ddmk::spatial_stream_occupancy(sa.W, sa.H, sa.pixel_bytes, &rps, &cps);
-        // per SM: one column CTA beside as many row CTAs as still fit (A/B: DDM_STREAM_R/C)
-        static const int env_r = std::getenv("DDM_STREAM_R") ? std::atoi(std::getenv("DDM_STREAM_R")) : 0;
-        static const int env_c = std::getenv("DDM_STREAM_C") ? std::atoi(std::getenv("DDM_STREAM_C")) : 0;
-        static const int env_ahead = std::getenv("DDM_STREAM_AHEAD") ? std::atoi(std::getenv("DDM_STREAM_AHEAD")) : 0;
-        const int cols_per_sm = env_c > 0 ? env_c : 1;
-        const int rows_per_sm = env_r > 0 ? env_r : std::max(1, std::min(2, rps - 1));
-        (void)cps;
-        const int ahead = env_ahead > 0 ? env_ahead : 3;
-        check(cudaEventRecord(chunk_events_[0], stream_), "cudaEventRecord");
-        check(cudaStreamWaitEvent(cols_stream_, chunk_events_[0], 0), "stream wait");
-        wait_frames(stream_, N);
-        check(ddmk::launch_spatial_warp_stream(sa, ctl, ahead, rows_per_sm * num_sms_, cols_per_sm * num_sms_,
-                                               stream_, cols_stream_), "streamed spatial pass");
-        check(cudaEventRecord(chunk_events_[1], cols_stream_), "cudaEventRecord");
-        check(cudaStreamWaitEvent(stream_, chunk_events_[1], 0), "join");
-        check(cudaMemcpyAsync(stream_flag_host(), ctl + 2, sizeof(unsigned), cudaMemcpyDeviceToHost, stream_),
-              "stream flag");
-        stream_flag_pending_ = true;
-        if (times) times->spatial_launches += 2;
-        return;
-    }
     // the row pass of chunk k+1 runs beside the column pass of chunk k on a second
     // stream, through two L2-resident `mid` buffers
     const bool overlap = warp_s && N > F && std::getenv("DDM_SPATIAL_SERIAL") == nullptr;
@@ -630,10 +565,10 @@ uint64_t Engine::run(const RunSpec& sp, PhaseTimes* times) {
         mark();
         if (sp.partial_mode && sp.on_partial) sp.on_partial(gi, ta.out, gc);
         // the host-side slot map / dest vectors must outlive the async copies
-        if (!sp.identity || sp.partial_mode) { check(cudaStreamSynchronize(stream_), "sync"); check_stream_flag(); }
+        if (!sp.identity || sp.partial_mode) check(cudaStreamSynchronize(stream_), "sync");
     }
     if (times) {
-        { check(cudaStreamSynchronize(stream_), "sync"); check_stream_flag(); }
+        check(cudaStreamSynchronize(stream_), "sync");
         for (size_t i = 0; i + 3 < evs.size(); i += 4) {
             float a = 0.f, b = 0.f;
             cudaEventElapsedTime(&a, evs[i], evs[i + 1]);
@@ -838,7 +773,7 @@ bool Engine::run_rings(const RunSpec& sp, const RingPlan& rp, double* d_means, P
         last_engines_ += "+radial";
         radial_means(static_cast<const double*>(m.d_out), L, m.out_stride, rc.flat_by_bin, rc.bin_off,
                      rp.nbins, d_means, stream_);
-        { check(cudaStreamSynchronize(stream_), "sync"); check_stream_flag(); }
+        check(cudaStreamSynchronize(stream_), "sync");
         return false;
     }
     // fused: spatial pass into the slot-major spectra, then the ring temporal launch
@@ -895,7 +830,7 @@ bool Engine::run_rings(const RunSpec& sp, const RingPlan& rp, double* d_means, P
         times->temporal_ms += b;
         times->temporal_launches += 2;
     }
-    if (!sp.identity) { check(cudaStreamSynchronize(stream_), "sync"); check_stream_flag(); }  // slot_of is host-side
+    if (!sp.identity) check(cudaStreamSynchronize(stream_), "sync");  // slot_of is host-side
     return true;
 }
 
@@ -949,7 +884,7 @@ void Engine::run_pairwise(const RunSpec& sp, PhaseTimes* times) {
                                                 num_sms_, stream_, lag0),
           "pairwise kernel");
     if (times) check(cudaEventRecord(ev_[3], stream_), "cudaEventRecord");
-    { check(cudaStreamSynchronize(stream_), "sync"); check_stream_flag(); }   // host lag / slot vectors
+    check(cudaStreamSynchronize(stream_), "sync");   // host lag / slot vectors
     if (times) {
         float a = 0.f, b = 0.f;
         cudaEventElapsedTime(&a, ev_[0], ev_[1]);
@@ -989,7 +924,7 @@ void Engine::spectra(const void* d_frames, int pixel_bytes, int W, int H, int N,
         check(f64 ? ddmk::launch_spatial<double>(sa, stream_) : ddmk::launch_spatial<float>(sa, stream_),
               "spatial kernels");
     }
-    { check(cudaStreamSynchronize(stream_), "sync"); check_stream_flag(); }
+    check(cudaStreamSynchronize(stream_), "sync");
 }
 
 void Engine::sequences(const void* d_seq, int64_t q, int64_t n, bool f64, double* d_out,
@@ -1078,7 +1013,7 @@ void Engine::sequences(const void* d_seq, int64_t q, int64_t n, bool f64, double
                                                            (int)n, d_mean, d_corr, d_da, d_aux);
         check(cudaGetLastError(), "restore kernel");
     }
-    { check(cudaStreamSynchronize(stream_), "sync"); check_stream_flag(); }
+    check(cudaStreamSynchronize(stream_), "sync");
 }
 
 }  // namespace ddm::b200

@@ -220,12 +220,6 @@ private:
     void wait_frames(cudaStream_t st, int frame_end);
     void* pinned_[2] = {nullptr, nullptr};
     size_t pinned_bytes_[2] = {0, 0};
-    // streamed spatial pass: its give-up flag lands in pinned memory; checked after the next
-    // synchronisation of stream_ (a set flag means the spectra are invalid)
-    unsigned* stream_flag_ = nullptr;
-    bool stream_flag_pending_ = false;
-    unsigned* stream_flag_host();
-    void check_stream_flag();   // call with stream_ drained
     std::mutex mu_;
     // last ring plan and its device copy (geometry only, reused across runs)
     struct RingCache {

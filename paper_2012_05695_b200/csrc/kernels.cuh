@@ -162,15 +162,7 @@ int spatial_warp_col_frames(int H);
 // parts: 1 = row pass (frames -> mid), 2 = column pass (mid -> spectra), 3 = both
 template <typename S>
 cudaError_t launch_spatial_warp(const SpatialArgs& a, cudaStream_t stream, int parts = 3);
-// Streamed register spatial step over a whole stack (spatial_warp.cu): persistent row and
-// column kernels side by side on two streams, the column pass consuming the row pass's output
-// from L2 chunk by chunk. ctl: spatial_stream_ctl_words(N, H) zeroed words; after completion
-// ctl[2] != 0 reports a column CTA that gave up waiting (results invalid).
-int spatial_stream_ctl_words(int N, int H);
-cudaError_t launch_spatial_warp_stream(const SpatialArgs& a, unsigned* ctl, int ahead, int rows_grid,
-                                       int cols_grid, cudaStream_t rows_st, cudaStream_t cols_st);
-// resident CTAs per SM of each streamed kernel alone (f32)
-void spatial_stream_occupancy(int W, int H, int pixel_bytes, int* rows_per_sm, int* cols_per_sm);
+
 
 // Shared memory / tile geometry chosen for the temporal kernel; the spectra layout T must
 // match it. Returns 0 when the sequence length is beyond what one CTA can hold.

@@ -17,7 +17,6 @@
 #include <type_traits>
 
 #include "kernels.cuh"
-#include "temporal_common.cuh"
 #include "warp_fft.cuh"
 
 namespace ddmk {
@@ -42,22 +41,12 @@ __host__ __device__ constexpr int split_a() {
 }
 
 // ---------------------------------------------------------------------------- rows
-// Row pitch (32-bit words) of the streamed kernel's shared-memory stage: one row of W pixels
-// plus 16 bytes, so the two row groups of a warp fall on different banks
-template <typename Pix, int L>
-__host__ __device__ constexpr int stage_pitch_words() {
-    return (2 * L * (int)sizeof(Pix)) / 4 + 4;
-}
-
-// stage != nullptr: the CTA's RB rows were staged by TMA bulk copies (pitch
-// stage_pitch_words) instead of being read from global memory
 template <typename S, typename Pix, int L>
 __device__ __forceinline__ void rows2_body(const Pix* __restrict__ frames, int H, int frame0,
                                            const cpx<S>* __restrict__ tw_row,
                                            const cpx<S>* __restrict__ tw_post,
                                            cpx<S>* __restrict__ mid, int item,
-                                           unsigned char* smem_raw,
-                                           const uint32_t* stage = nullptr) {
+                                           unsigned char* smem_raw) {
     constexpr int A = split_a<L>(), B = L / A;
     constexpr int W = 2 * L, Wh = L + 1;
     constexpr int RB = kThreads / A;                 // rows per CTA (one per group)
@@ -79,19 +68,16 @@ __device__ __forceinline__ void rows2_body(const Pix* __restrict__ frames, int H
         const Pix* row = frames + ((size_t)(frame0 + fi) * H + r0 + g) * W;
         if constexpr (std::is_same_v<Pix, uint16_t>) {
             const uint32_t* w32 = reinterpret_cast<const uint32_t*>(row);
-            const uint32_t* s32 = stage + g * stage_pitch_words<Pix, L>();
 #pragma unroll
             for (int b = 0; b < B; ++b) {
-                // read once: evict first
-                const uint32_t p = stage ? s32[a + A * b] : __ldcs(w32 + a + A * b);
+                const uint32_t p = __ldcs(w32 + a + A * b);   // read once: evict first
                 v[b] = {(S)(p & 0xFFFFu), (S)(p >> 16)};
             }
         } else {
             const uint16_t* w16 = reinterpret_cast<const uint16_t*>(row);
-            const uint16_t* s16 = reinterpret_cast<const uint16_t*>(stage + g * stage_pitch_words<Pix, L>());
 #pragma unroll
             for (int b = 0; b < B; ++b) {
-                const uint16_t p = stage ? s16[a + A * b] : __ldcs(w16 + a + A * b);
+                const uint16_t p = __ldcs(w16 + a + A * b);
                 v[b] = {(S)(p & 0xFFu), (S)(p >> 8)};
             }
         }
@@ -238,8 +224,7 @@ __device__ __forceinline__ void cols2_core(const cpx<S>* __restrict__ mid, int W
     cpx<S> v[B];
     if (g < nf) {
         const cpx<S>* col = mid + ((size_t)(f0 + g) * Wh + c) * HL;
-        // L2 loads (ld.global.cg): in the streamed pass another SM wrote these lines moments
-        // ago, and they are read exactly once
+        // L2 loads (ld.global.cg): read exactly once
 #pragma unroll
         for (int b = 0; b < B; ++b) v[b] = ld_cg(col + a + A * b);
         group_fft<A, B, -1, S>(v, sm + g * REG, a, tw);
@@ -310,146 +295,6 @@ __host__ __device__ constexpr size_t cols_smem(size_t cs) {
     return (ex > st ? ex : st) * cs;
 }
 
-// ---------------------------------------------------------------------------- streamed
-// One persistent row kernel and one persistent column kernel run side by side (two streams)
-// over the whole stack. Work is handed out in order by ticket counters; the column CTA of
-// (chunk k of F frames, column c) starts once every row item of chunk k has been written,
-// so it reads `mid` lines another SM wrote moments earlier, from L2, and discards them
-// (no write-back). Row CTAs run at most R chunks ahead of the column pass (a soft limit: after
-// a bounded wait they proceed, which only costs L2 residency, never correctness: `mid` spans
-// the whole stack). Control words (StreamCtl::ctl, zeroed before the launch):
-//   [0] row ticket, [1] column ticket, [2] error (a column CTA gave up waiting),
-//   [4 + k] row items done in chunk k, [4 + nchunks + k] column items done in chunk k.
-struct StreamCtl {
-    unsigned* ctl = nullptr;
-    int nchunks = 0;
-    int ahead = 4;          // R
-};
-
-__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
-    unsigned v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-
-constexpr int kSoftSpins = 512;        // x >= 128 ns: the row pass's wait for the column pass
-constexpr long kHardSpins = 1l << 24;  // x >= 64 ns: > 1 s, only a broken launch gets here
-
-// Row CTAs prefetch their next item's RB rows (RB x W pixels, contiguous in the frame) into a
-// second shared-memory stage by TMA bulk copies while transforming the current item: the row
-// pass streams the frames from HBM with few warps per SM (it shares the SM with the column
-// pass), so the loads must not wait on the warps.
-template <typename Pix, int L>
-__host__ __device__ constexpr size_t rows_stage_bytes() {
-    return (size_t)(kThreads / split_a<L>()) * stage_pitch_words<Pix, L>() * 4;
-}
-
-// <= 64 registers at the headline's row length, so two row CTAs and one column CTA (<= 128)
-// share an SM's register file
-template <int L>
-constexpr int rows_stream_min_blocks() { return L <= 256 ? 4 : 2; }
-
-template <typename S, typename Pix, int L>
-__global__ void __launch_bounds__(kThreads, rows_stream_min_blocks<L>())
-rows2_stream_kernel(const Pix* __restrict__ frames, int H, int N, const cpx<S>* __restrict__ tw_row,
-                    const cpx<S>* __restrict__ tw_post, cpx<S>* __restrict__ mid, int Fc,
-                    const StreamCtl sc) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ int s_item[2];
-    __shared__ __align__(8) unsigned long long bar[2];
-    constexpr int RB = kThreads / split_a<L>();
-    constexpr int Wh = L + 1;
-    constexpr int W = 2 * L;
-    constexpr size_t kRowsArea = (rows_smem<L>(sizeof(cpx<S>)) + 127) / 128 * 128;
-    constexpr size_t kStage = rows_stage_bytes<Pix, L>();
-    auto stage = [&](int buf) { return reinterpret_cast<uint32_t*>(smem_raw + kRowsArea + buf * kStage); };
-    const int rblocks = H / RB;
-    const int nitems = N * rblocks, per_chunk = Fc * rblocks;
-    unsigned* rows_done = sc.ctl + 4;
-    const unsigned* cols_done = sc.ctl + 4 + sc.nchunks;
-
-    // thread 0: take the next ticket, hold it back while the column pass is `ahead` chunks
-    // behind (bounded), start its rows' bulk copies into stage[buf]
-    auto fetch = [&](int buf) -> int {
-        const int it = (int)atomicAdd(sc.ctl, 1u);
-        if (it >= nitems) return it;
-        const int k = it / per_chunk;
-        if (k >= sc.ahead)
-            for (int spin = 0; spin < kSoftSpins && ld_acquire(cols_done + k - sc.ahead) < (unsigned)Wh; ++spin)
-                __nanosleep(128);
-        const int fi = it / rblocks, r0 = (it - fi * rblocks) * RB;
-        const Pix* src = frames + ((size_t)fi * H + r0) * W;
-        tc::fence_expect(&bar[buf], (uint32_t)(RB * W * sizeof(Pix)));
-        for (int r = 0; r < RB; ++r)
-            tc::bulk_copy(stage(buf) + r * stage_pitch_words<Pix, L>(), src + (size_t)r * W,
-                          (uint32_t)(W * sizeof(Pix)), &bar[buf]);
-        return it;
-    };
-
-    if (threadIdx.x == 0) {
-        tc::mbar_init(&bar[0]);
-        tc::mbar_init(&bar[1]);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        s_item[0] = fetch(0);
-    }
-    __syncthreads();
-    uint32_t phases = 0u;   // bit b: parity of stage b's barrier
-    for (int buf = 0;; buf ^= 1) {
-        const int item = s_item[buf];
-        if (item >= nitems) break;
-        // the other stage was released by the previous iteration's final barrier
-        if (threadIdx.x == 0) s_item[buf ^ 1] = fetch(buf ^ 1);
-        tc::mbar_wait(&bar[buf], (phases >> buf) & 1u);
-        phases ^= 1u << buf;
-        rows2_body<S, Pix, L>(frames, H, 0, tw_row, tw_post, mid, item, smem_raw, stage(buf));
-        __syncthreads();  // every thread's mid stores (and stage reads) precede the release below
-        if (threadIdx.x == 0) {
-            __threadfence();
-            atomicAdd(rows_done + item / per_chunk, 1u);
-        }
-    }
-}
-
-template <typename S, int HL>
-__global__ void __launch_bounds__(kThreads)
-cols2_stream_kernel(const cpx<S>* __restrict__ mid, int Wh, int N, int rblocks,
-                    const cpx<S>* __restrict__ tw_col, cpx<S>* __restrict__ spec, SpecLayout lay,
-                    const int* __restrict__ slot_of_flat, const __grid_constant__ PeerTable peers,
-                    const StreamCtl sc) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ int s_item;
-    constexpr int F = kThreads / split_a<HL>();
-    const int nitems = sc.nchunks * Wh;
-    const unsigned* rows_done = sc.ctl + 4;
-    unsigned* cols_done = sc.ctl + 4 + sc.nchunks;
-    for (;;) {
-        if (threadIdx.x == 0) {
-            int it = (int)atomicAdd(sc.ctl + 1, 1u);
-            if (it < nitems) {
-                const int k = it / Wh;
-                const unsigned want = (unsigned)(min(F, N - k * F) * rblocks);
-                long spin = 0;
-                while (ld_acquire(rows_done + k) < want) {
-                    __nanosleep(64);
-                    if (++spin > kHardSpins || ld_acquire(sc.ctl + 2) != 0u) {
-                        atomicExch(sc.ctl + 2, 1u);
-                        it = nitems;
-                        break;
-                    }
-                }
-            }
-            s_item = it;
-        }
-        __syncthreads();
-        const int item = s_item;
-        if (item >= nitems) break;
-        const int k = item / Wh, c = item - k * Wh;
-        cols2_core<S, HL>(mid, Wh, N, 0, N, tw_col, spec, lay, slot_of_flat, peers, c, k * F, smem_raw);
-        __syncthreads();
-        if (threadIdx.x == 0) atomicAdd(cols_done + k, 1u);
-    }
-}
-
 template <typename S, typename Pix, int L>
 cudaError_t launch_rows2(const SpatialArgs& a, cudaStream_t st) {
     auto k = rows2_kernel<S, Pix, L>;
@@ -478,33 +323,6 @@ cudaError_t launch_cols2(const SpatialArgs& a, cudaStream_t st) {
                                     a.nframes, static_cast<const cpx<S>*>(a.tw_col.ptr),
                                     static_cast<cpx<S>*>(a.spec), a.layout,
                                     a.slot_of_flat, a.peers);
-    return cudaGetLastError();
-}
-
-template <typename S, typename Pix, int L>
-cudaError_t launch_rows2_stream(const SpatialArgs& a, const StreamCtl& sc, int Fc, int grid,
-                                cudaStream_t st) {
-    auto k = rows2_stream_kernel<S, Pix, L>;
-    const size_t smem = (rows_smem<L>(sizeof(cpx<S>)) + 127) / 128 * 128 + 2 * rows_stage_bytes<Pix, L>();
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    k<<<grid, kThreads, smem, st>>>(static_cast<const Pix*>(a.frames), a.H, a.N,
-                                    static_cast<const cpx<S>*>(a.tw_row.ptr),
-                                    static_cast<const cpx<S>*>(a.tw_post.ptr),
-                                    static_cast<cpx<S>*>(a.mid), Fc, sc);
-    return cudaGetLastError();
-}
-
-template <typename S, int HL>
-cudaError_t launch_cols2_stream(const SpatialArgs& a, const StreamCtl& sc, int rblocks, int grid,
-                                cudaStream_t st) {
-    auto k = cols2_stream_kernel<S, HL>;
-    const size_t smem = cols_smem<HL>(sizeof(cpx<S>));
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    k<<<grid, kThreads, smem, st>>>(static_cast<const cpx<S>*>(a.mid), a.W / 2 + 1, a.N, rblocks,
-                                    static_cast<const cpx<S>*>(a.tw_col.ptr),
-                                    static_cast<cpx<S>*>(a.spec), a.layout, a.slot_of_flat, a.peers, sc);
     return cudaGetLastError();
 }
 
@@ -555,82 +373,5 @@ cudaError_t launch_spatial_warp(const SpatialArgs& a, cudaStream_t stream, int p
 }
 
 template cudaError_t launch_spatial_warp<float>(const SpatialArgs&, cudaStream_t, int);
-
-int spatial_stream_ctl_words(int N, int H) {
-    const int Fc = spatial_warp_col_frames(H);
-    return 4 + 2 * ((N + Fc - 1) / Fc);
-}
-
-// The streamed spatial step over the whole stack (a.frame0 = 0, a.nframes = N, a.mid spans
-// N frames): rows on `rows_st`, columns on `cols_st`, both persistent; ctl zeroed by the
-// caller (spatial_stream_ctl_words(N, H) words).
-cudaError_t launch_spatial_warp_stream(const SpatialArgs& a, unsigned* ctl, int ahead, int rows_grid,
-                                       int cols_grid, cudaStream_t rows_st, cudaStream_t cols_st) {
-    const int L = a.W / 2;
-    const int Fc = spatial_warp_col_frames(a.H);
-    StreamCtl sc;
-    sc.ctl = ctl;
-    sc.nchunks = (a.N + Fc - 1) / Fc;
-    sc.ahead = ahead;
-    const int e = 31 - __builtin_clz(L);
-    const int RB = kThreads / std::min(1 << (e / 2), 32);
-    const int rblocks = a.H / RB;
-    cudaError_t err = cudaSuccess;
-#define DDMK_R2S(LEN)                                                                              \
-    case LEN:                                                                                      \
-        err = a.pixel_bytes == 2 ? launch_rows2_stream<float, uint16_t, LEN>(a, sc, Fc, rows_grid, rows_st) \
-                                 : launch_rows2_stream<float, uint8_t, LEN>(a, sc, Fc, rows_grid, rows_st); \
-        break;
-    switch (L) {
-        DDMK_R2S(16) DDMK_R2S(32) DDMK_R2S(64) DDMK_R2S(128) DDMK_R2S(256) DDMK_R2S(512) DDMK_R2S(1024)
-    default: return cudaErrorInvalidValue;
-    }
-#undef DDMK_R2S
-    if (err != cudaSuccess) return err;
-#define DDMK_C2S(LEN) \
-    case LEN: err = launch_cols2_stream<float, LEN>(a, sc, rblocks, cols_grid, cols_st); break;
-    switch (a.H) {
-        DDMK_C2S(16) DDMK_C2S(32) DDMK_C2S(64) DDMK_C2S(128) DDMK_C2S(256) DDMK_C2S(512) DDMK_C2S(1024)
-        DDMK_C2S(2048)
-    default: return cudaErrorInvalidValue;
-    }
-#undef DDMK_C2S
-    return err;
-}
-
-// CTAs of each streamed kernel that fit one SM beside `other` CTAs of the other one
-void spatial_stream_occupancy(int W, int H, int pixel_bytes, int* rows_per_sm, int* cols_per_sm) {
-    const int L = W / 2;
-    int r = 0, c = 0;
-    auto occ = [](auto kern, size_t smem) {
-        int n = 0;
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, kThreads, smem);
-        return n;
-    };
-#define DDMK_OR(LEN)                                                                      \
-    case LEN:                                                                             \
-        r = pixel_bytes == 2 ? occ(rows2_stream_kernel<float, uint16_t, LEN>,                \
-                                   (rows_smem<LEN>(8) + 127) / 128 * 128 + 2 * rows_stage_bytes<uint16_t, LEN>()) \
-                             : occ(rows2_stream_kernel<float, uint8_t, LEN>,                 \
-                                   (rows_smem<LEN>(8) + 127) / 128 * 128 + 2 * rows_stage_bytes<uint8_t, LEN>()); \
-        break;
-    switch (L) {
-        DDMK_OR(16) DDMK_OR(32) DDMK_OR(64) DDMK_OR(128) DDMK_OR(256) DDMK_OR(512) DDMK_OR(1024)
-    default: break;
-    }
-#undef DDMK_OR
-#define DDMK_OC(LEN) \
-    case LEN: c = occ(cols2_stream_kernel<float, LEN>, cols_smem<LEN>(8)); break;
-    switch (H) {
-        DDMK_OC(16) DDMK_OC(32) DDMK_OC(64) DDMK_OC(128) DDMK_OC(256) DDMK_OC(512) DDMK_OC(1024)
-        DDMK_OC(2048)
-    default: break;
-    }
-#undef DDMK_OC
-    *rows_per_sm = r;
-    *cols_per_sm = c;
-}
-
 
 }  // namespace ddmk
