@@ -93,6 +93,34 @@ int ddm_b200_run_u8(const uint8_t* pixels, int width, int height, int frames,
                     double* out_values, int64_t out_capacity, int64_t* out_lags,
                     int64_t* out_n_lags, ddm_b200_counters* counters,
                     ddm_b200_timing* timing);
+/* Opaque staging session (SURVEY.md §8b "Required C-ABI"). The reference re-reads and
+   re-transforms the frames on every ddm::run (scheduler.cpp:413-483); a session holds one
+   stack in HBM and runs the WITH_FT branch over it for any number of wave-vector / lag
+   requests. Each session owns its own device buffers and streams (its own engine, not the
+   per-device one behind ddm_b200_run_*), so sessions on one GPU run concurrently; use one
+   session from one thread at a time. One GPU per session: multi-GPU runs are one process per
+   GPU (ddm_b200_shard_plan and the *_shard_* entries). */
+typedef struct ddm_b200 ddm_b200;
+/* precision 0 = f32, 1 = f64; device = CUDA ordinal */
+int ddm_b200_create(int width, int height, int frames, int precision, int device, ddm_b200** out);
+int ddm_b200_destroy(ddm_b200* session);
+/* frames [first, first + count) of a frame-major host buffer holding exactly those frames
+   (FrameSource::read_frame, frame_source.hpp:33); u16 or u8, not mixed within a session */
+int ddm_b200_stage_frames(ddm_b200* session, const uint16_t* host, int first, int count);
+int ddm_b200_stage_frames_u8(ddm_b200* session, const uint8_t* host, int first, int count);
+/* WITH_FT over the staged stack (every frame must be staged). wv_flat: q_count ascending flat
+   indices row * (width/2+1) + col (NULL = the whole half plane, q_count ignored); lags: NULL/0
+   = every lag, else normalised like RunConfig::lags. out_lag_major: n_lags x height x
+   (width/2+1) f64, zeros outside wv_flat, d(0) = 0 (ResultMap, result_map.hpp:12-32);
+   validate() floors (archive.cpp:44-58); counters spatial_ffts = frames, temporal_ffts =
+   2 q_count. A page-locked out_lag_major streams out beside the temporal pass. */
+int ddm_b200_run_with_ft(ddm_b200* session, const int64_t* wv_flat, int64_t q_count,
+                         const int64_t* lags, int64_t n_lags, double* out_lag_major,
+                         int64_t out_capacity, ddm_b200_counters* counters,
+                         ddm_b200_timing* timing);
+/* the kernels the session's last run selected (like ddm_b200_last_engines) */
+int ddm_b200_session_engines(ddm_b200* session, char* buf, int64_t capacity);
+
 /* ddm::run over RawStackFileSource (frame_source.cpp:27-78) */
 int ddm_b200_run_raw_stack(const char* path, const ddm_b200_run_config* config,
                            double* out_values, int64_t out_capacity, int64_t* out_lags,

@@ -11,6 +11,7 @@
 #include "ddm/synth.hpp"
 #include "ddm/temporal.hpp"
 #include "run_internal.hpp"
+#include "session.hpp"
 
 #include <algorithm>
 #include <cmath>
@@ -938,6 +939,72 @@ int ddm_b200_generate_device(int64_t particles, double diffusion, double psf_sig
         c.frame_interval = frame_interval;
         c.seed = seed;
         ddm::generate_device(c, d_out, device, stream);
+    });
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------- sessions
+struct ddm_b200 {
+    ddm::detail::Session s;
+    ddm_b200(int w, int h, int n, int p, int d) : s(w, h, n, p, d) {}
+};
+
+extern "C" {
+
+int ddm_b200_create(int width, int height, int frames, int precision, int device, ddm_b200** out) {
+    return guarded([&] {
+        if (!out) throw ddm::InputError("null session pointer");
+        *out = nullptr;
+        *out = ddm::detail::guard_device([&] { return new ddm_b200(width, height, frames, precision, device); });
+    });
+}
+
+int ddm_b200_destroy(ddm_b200* session) {
+    return guarded([&] { delete session; });
+}
+
+int ddm_b200_stage_frames(ddm_b200* session, const uint16_t* host, int first, int count) {
+    return guarded([&] {
+        if (!session) throw ddm::InputError("null session");
+        ddm::detail::guard_device([&] {
+            session->s.stage(host, 2, first, count);
+            return 0;
+        });
+    });
+}
+
+int ddm_b200_stage_frames_u8(ddm_b200* session, const uint8_t* host, int first, int count) {
+    return guarded([&] {
+        if (!session) throw ddm::InputError("null session");
+        ddm::detail::guard_device([&] {
+            session->s.stage(host, 1, first, count);
+            return 0;
+        });
+    });
+}
+
+int ddm_b200_run_with_ft(ddm_b200* session, const int64_t* wv_flat, int64_t q_count, const int64_t* lags,
+                         int64_t n_lags, double* out_lag_major, int64_t out_capacity,
+                         ddm_b200_counters* counters, ddm_b200_timing* timing) {
+    return guarded([&] {
+        if (!session) throw ddm::InputError("null session");
+        ddm::RunCounters c;
+        const ddm::TimingBreakdown t = ddm::detail::guard_device([&] {
+            return session->s.run_with_ft(wv_flat, q_count, lags, n_lags, out_lag_major, out_capacity, &c);
+        });
+        if (counters) *counters = {c.spatial_ffts, c.temporal_ffts, c.pairs};
+        if (timing) *timing = {t.disk, t.step1, t.step2, t.merge, t.other, t.total};
+    });
+}
+
+int ddm_b200_session_engines(ddm_b200* session, char* buf, int64_t capacity) {
+    return guarded([&] {
+        if (!session || !buf || capacity < 1) throw ddm::InputError("null session or buffer");
+        const std::string& e = session->s.last_engines();
+        const std::size_t n = std::min<std::size_t>(e.size(), std::size_t(capacity - 1));
+        std::memcpy(buf, e.data(), n);
+        buf[n] = '\0';
     });
 }
 

@@ -78,6 +78,13 @@ def lib():
         L.ddm_b200_pad_length.argtypes = [C.c_int64]
         L.ddm_b200_max_frames.restype = C.c_int64
         L.ddm_b200_max_frames.argtypes = [C.c_int]
+        L.ddm_b200_create.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]
+        L.ddm_b200_destroy.argtypes = [C.c_void_p]
+        L.ddm_b200_stage_frames.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int]
+        L.ddm_b200_stage_frames_u8.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int]
+        L.ddm_b200_run_with_ft.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
+                                           C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]
+        L.ddm_b200_session_engines.argtypes = [C.c_void_p, C.c_char_p, C.c_int64]
         L.ddm_b200_run_device.argtypes = [
             C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int64),
             C.c_int64, C.c_int, C.c_double, C.c_void_p, C.c_int, C.c_int, C.c_void_p,
@@ -248,6 +255,72 @@ def run(stack, config: RunConfig, frame_interval: float = 1.0) -> ResultArchive:
                          config.workers,
                          {f: int(getattr(counters, f)) for f, _ in Counters._fields_},
                          {f: float(getattr(timing, f)) for f, _ in Timing._fields_})
+
+
+class Session:
+    """Opaque staging session (`ddm_b200_create` / `_stage_frames` / `_run_with_ft`,
+    SURVEY.md §8b): one stack resident in HBM, any number of WITH_FT runs over it, each with
+    the reference WithFt branch's contract (`scheduler.cpp:413-483`). Owns its own device
+    engine, so sessions on one GPU run concurrently; use one from one thread at a time."""
+
+    def __init__(self, width: int, height: int, frames: int, precision: str = "f32", device: int = 0):
+        if precision not in ("f32", "f64"):
+            raise InputError(f"unknown precision '{precision}'")
+        self.width, self.height, self.frames = int(width), int(height), int(frames)
+        h = C.c_void_p()
+        _check(lib().ddm_b200_create(self.width, self.height, self.frames,
+                                     0 if precision == "f32" else 1, int(device), C.byref(h)))
+        self._h = h
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None and self._h.value:
+            _check(lib().ddm_b200_destroy(self._h))
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def stage(self, frames, first: int = 0) -> None:
+        """frames [first, first + len(frames)) from a [count, H, W] uint16 or uint8 array"""
+        st = np.asarray(frames)
+        if st.ndim != 3 or st.shape[1:] != (self.height, self.width):
+            raise InputError("frames must be [count, height, width] of the session's frame size")
+        u8 = st.dtype == np.uint8
+        st = np.ascontiguousarray(st, dtype=np.uint8 if u8 else np.uint16)
+        fn = lib().ddm_b200_stage_frames_u8 if u8 else lib().ddm_b200_stage_frames
+        _check(fn(self._h, _p(st, C.c_uint8 if u8 else C.c_uint16), int(first), int(st.shape[0])))
+
+    def run_with_ft(self, wave_vectors=None, lags=()):
+        """-> (map [n_lags, H, W/2+1] f64, counters, timing). wave_vectors: ascending flat
+        indices (None = the whole half plane); lags: empty = every lag."""
+        plane = self.height * half_cols(self.width)
+        wv = None if wave_vectors is None else np.ascontiguousarray(np.asarray(wave_vectors), dtype=np.int64)
+        lg = np.ascontiguousarray(np.asarray(list(lags), dtype=np.int64))
+        n_out = len(np.unique(lg)) if len(lg) else self.frames
+        values = np.empty(max(n_out, 1) * plane)
+        counters, timing = Counters(), Timing()
+        _check(lib().ddm_b200_run_with_ft(
+            self._h, _p(wv, C.c_int64) if wv is not None else None,
+            C.c_int64(0 if wv is None else wv.size), _p(lg, C.c_int64) if len(lg) else None,
+            C.c_int64(len(lg)), _p(values, C.c_double), C.c_int64(values.size), C.byref(counters),
+            C.byref(timing)))
+        return (values[: n_out * plane].reshape(n_out, self.height, half_cols(self.width)),
+                {f: int(getattr(counters, f)) for f, _ in Counters._fields_},
+                {f: float(getattr(timing, f)) for f, _ in Timing._fields_})
+
+    def engines(self) -> str:
+        buf = C.create_string_buffer(256)
+        _check(lib().ddm_b200_session_engines(self._h, buf, C.c_int64(256)))
+        return buf.value.decode()
 
 
 def run_raw_stack(path: str, config: RunConfig) -> ResultArchive:
