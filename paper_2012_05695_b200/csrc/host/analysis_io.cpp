@@ -75,6 +75,27 @@ std::vector<ExponentialFit> fit_all_bins_on(const RadialProfile& p, int device) 
 
 std::vector<ExponentialFit> fit_all_bins(const RadialProfile& p) { return fit_all_bins_on(p, 0); }
 
+ExponentialFit fit_exponential(const RadialProfile& p, std::int64_t q_bin) {
+    if (q_bin < 0 || q_bin >= p.bin_count) throw InputError("fit_exponential: bin out of range");
+    if (p.counts[std::size_t(q_bin)] < 1) throw InputError("fit_exponential: empty bin");
+    RadialProfile one;
+    one.bin_count = 1;
+    one.frame_interval = p.frame_interval;
+    one.lags = p.lags;
+    one.counts = {p.counts[std::size_t(q_bin)]};
+    one.means.resize(p.lags.size());
+    std::size_t usable = 0;
+    for (std::size_t li = 0; li < p.lags.size(); ++li) {
+        one.means[li] = p.mean(std::int64_t(li), q_bin);
+        if (p.lags[li] >= 1 && std::isfinite(one.means[li])) ++usable;
+    }
+    if (usable < 4) throw InputError("fit_exponential: need at least 4 usable lags");
+    auto fits = fit_all_bins_on(one, 0);
+    if (fits.empty()) throw InputError("fit_exponential: need at least 4 usable lags");
+    fits.front().q_bin = q_bin;
+    return fits.front();
+}
+
 DiffusionEstimate estimate_diffusion(const std::vector<ExponentialFit>& fits, std::int64_t width,
                                      std::int64_t q_lo, std::int64_t q_hi) {
     if (width < 1) throw InputError("estimate_diffusion: bad width");

@@ -98,6 +98,24 @@ ImageStack load_stack(const fs::path& path, StackFormat format) {
     return st;
 }
 
+void write_pgm(std::span<const std::uint16_t> frame, int width, int height, const fs::path& path) {
+    if (width < 1 || height < 1 || std::size_t(width) * std::size_t(height) != frame.size())
+        throw InputError("write_pgm: frame size does not match dimensions");
+    char head[64];
+    const int hn = std::snprintf(head, sizeof head, "P5\n%d %d\n65535\n", width, height);
+    std::vector<unsigned char> bytes(std::size_t(hn) + 2 * frame.size());
+    std::memcpy(bytes.data(), head, std::size_t(hn));
+    unsigned char* px = bytes.data() + hn;
+    for (const std::uint16_t v : frame) {   // big-endian samples (maxval > 255)
+        *px++ = static_cast<unsigned char>(v >> 8);
+        *px++ = static_cast<unsigned char>(v & 0xFFu);
+    }
+    std::ofstream out(path, std::ios::binary | std::ios::trunc);
+    if (!out) throw IoError("cannot create " + path.string());
+    out.write(reinterpret_cast<const char*>(bytes.data()), std::streamsize(bytes.size()));
+    if (!out) throw IoError("short write to " + path.string());
+}
+
 void write_raw_stack(const ImageStack& stack, const fs::path& path) {
     // one JSON header line, then the samples as u16 little-endian (`image_stack.cpp:223-247`)
     stack.validate();
