@@ -8,7 +8,7 @@
 // s = w. (The one-group engine runs R/2 of its warps idle through the inverse.)
 //
 // Per group, per sequence (group-local named barriers; the other group is never waited on):
-//   TMA bulk copy of t -> stage; mean; 2 x (build y_r, FFT_1024, P_r -> pu)
+//   TMA bulk copy of t -> stage; mean; shift written back; 2 x (build y_r, FFT_1024, P_r -> pu)
 //   |t|^2 -> scratch (natural order), suffix sums S(m) -> stage (t is dead)
 //   inverse: E_w = IFFT_1024(P_2w + i P_2w+1), twisted, written over P_2w / P_2w+1 in place
 //   U(m' + 1024 p) = sum_s E'_s(m') e^{2 pi i s p / H}, in place; unfold; d(m) -> out
@@ -204,6 +204,12 @@ temporal_long2_kernel(const cpx<float>* __restrict__ spec, const __grid_constant
         }
         mx *= inv_nf;
         my *= inv_nf;
+        // shift once and write t back: the forward transforms and |t|^2 read it shifted
+        for (int n = gtid; n < N; n += TG) {
+            const cpx<float> x = stage[n];
+            stage[n] = {x.x - mx, x.y - my};
+        }
+        group_bar(bid, TG);
 
         // ---- forward: this warp's two residues r = w and r = w + G
 #pragma unroll 1
@@ -222,7 +228,7 @@ temporal_long2_kernel(const cpx<float>* __restrict__ spec, const __grid_constant
                 for (int j = 0; j < H; ++j) {
                     const int n = n1 + kF2 * j;
                     if (FULL || n < N) {
-                        const cpx<float> t = {stage[n].x - mx, stage[n].y - my};
+                        const cpx<float> t = stage[n];
                         a = (j == 0) ? t : cadd(a, cmul(t, wj[j]));
                     }
                 }
@@ -239,8 +245,8 @@ temporal_long2_kernel(const cpx<float>* __restrict__ spec, const __grid_constant
         for (int n = gtid; n < G2::NMAX; n += TG) {
             float p = 0.f;
             if (FULL || n < N) {
-                const float tx = stage[n].x - mx, ty = stage[n].y - my;
-                p = tx * tx + ty * ty;
+                const cpx<float> x = stage[n];
+                p = x.x * x.x + x.y * x.y;
             }
             pw[pad32b(n)] = p;
         }
@@ -287,9 +293,14 @@ temporal_long2_kernel(const cpx<float>* __restrict__ spec, const __grid_constant
             }
             __syncwarp();
             fft1024<+1, false>(v, my_scratch, lane, tw_even);
+            if (w == 0) {   // twist e^{2 pi i 0 m' / L} = 1
 #pragma unroll
-            for (int d = 0; d < 32; ++d)
-                pu[w * kF2 + lane + 32 * d] = cmul(v[d], cmul(comb_lane, comb_d[w * 32 + d]));
+                for (int d = 0; d < 32; ++d) pu[lane + 32 * d] = v[d];
+            } else {
+#pragma unroll
+                for (int d = 0; d < 32; ++d)
+                    pu[w * kF2 + lane + 32 * d] = cmul(v[d], cmul(comb_lane, comb_d[w * 32 + d]));
+            }
         }
         group_bar(bid, TG);
 
