@@ -546,7 +546,10 @@ uint64_t Engine::run(const RunSpec& sp, PhaseTimes* times) {
                 check(ddmk::launch_temporal_warp(tc, num_sms_, stream_), "temporal kernel");
                 check(cudaEventRecord(d2h_events_[c + 2], stream_), "cudaEventRecord");
                 check(cudaStreamWaitEvent(d2h_stream_, d2h_events_[c + 2], 0), "stream wait");
-                if (c == 0) check(cudaEventRecord(d2h_events_[0], d2h_stream_), "cudaEventRecord");
+                if (c == 0) {
+                    check(cudaEventRecord(d2h_events_[0], d2h_stream_), "cudaEventRecord");
+                    d2h_pending_ = true;   // from here on a failure must still drain the copies
+                }
                 const size_t pitch = (size_t)ta.out_stride * ob;
                 check(cudaMemcpy2DAsync(static_cast<char*>(sp.host_out) + (size_t)(gb + qa) * ob, pitch,
                                         tc.out, pitch, (size_t)(qb - qa) * ob, sp.lags.size(),
@@ -554,7 +557,6 @@ uint64_t Engine::run(const RunSpec& sp, PhaseTimes* times) {
                       "map chunk copy");
             }
             check(cudaEventRecord(d2h_events_[1], d2h_stream_), "cudaEventRecord");
-            d2h_pending_ = true;
             if (times) times->temporal_launches += chunks;
         } else {
             check(warp_t ? ddmk::launch_temporal_warp(ta, num_sms_, stream_)
