@@ -102,8 +102,10 @@ constexpr int kXS = 32 * kXP;
 template <int SIGN, bool ODD>
 __device__ __forceinline__ void fft1024(cpx<float> (&v)[32], cpx<float>* scratch, int lane,
                                         const cpx<float>* __restrict__ twt) {
-    if constexpr (ODD) premul_w64<SIGN>(v);
-    RegDft<32, SIGN, float>::run(v);
+    if constexpr (ODD)   // W_64^{b} fused into the first butterflies (compile-time constants)
+        dft32_fused<SIGN, float, true>(v, [](int b) { return ct_w<SIGN, float>(b, 64); });
+    else
+        RegDft<32, SIGN, float>::run(v);
 #pragma unroll
     for (int c = 0; c < 32; ++c) scratch[c * kXP + lane] = v[c];
     __syncwarp();
