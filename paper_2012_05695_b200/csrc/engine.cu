@@ -366,10 +366,12 @@ void Engine::spatial_pass(ddmk::SpatialArgs sa, bool f64, bool warp_s, PhaseTime
             // the buffer is free once the column pass of chunk k-2 has read it
             if (k >= 2) check(cudaStreamWaitEvent(stream_, chunk_events_[2 * (k - 2) + 1], 0), "wait");
             wait_frames(stream_, sa.frame0 + sa.nframes);
-            check(ddmk::launch_spatial_warp<float>(sa, stream_, 1), "row pass");
+            check(f64 ? ddmk::launch_spatial_warp<double>(sa, stream_, 1)
+                      : ddmk::launch_spatial_warp<float>(sa, stream_, 1), "row pass");
             check(cudaEventRecord(rows_done, stream_), "cudaEventRecord");
             check(cudaStreamWaitEvent(cols_stream_, rows_done, 0), "wait");
-            check(ddmk::launch_spatial_warp<float>(sa, cols_stream_, 2), "column pass");
+            check(f64 ? ddmk::launch_spatial_warp<double>(sa, cols_stream_, 2)
+                      : ddmk::launch_spatial_warp<float>(sa, cols_stream_, 2), "column pass");
             check(cudaEventRecord(cols_done, cols_stream_), "cudaEventRecord");
             if (times) times->spatial_launches += 2;
         }
@@ -379,7 +381,8 @@ void Engine::spatial_pass(ddmk::SpatialArgs sa, bool f64, bool warp_s, PhaseTime
             sa.frame0 = f0;
             sa.nframes = std::min(F, N - f0);
             wait_frames(stream_, f0 + sa.nframes);
-            check(warp_s ? ddmk::launch_spatial_warp<float>(sa, stream_)
+            check(warp_s ? (f64 ? ddmk::launch_spatial_warp<double>(sa, stream_)
+                              : ddmk::launch_spatial_warp<float>(sa, stream_))
                   : f64 ? ddmk::launch_spatial<double>(sa, stream_)
                         : ddmk::launch_spatial<float>(sa, stream_), "spatial kernels");
             if (times) times->spatial_launches += 2;
@@ -439,8 +442,12 @@ uint64_t Engine::run(const RunSpec& sp, PhaseTimes* times) {
     for (auto& g : sp.groups) gmax = std::max(gmax, g.second - g.first);
     const int64_t tiles_max = (gmax + T - 1) / T;
     void* d_spec = spec_.ensure((size_t)tiles_max * N * T * cs);
-    const bool warp_s = (warp_t || long_t) && ddmk::spatial_warp_supported(W, H, sp.pixel_bytes, sb) &&
+    // f64 on register-friendly frames: the f64 register spatial kernels write q-major spectra
+    // that the generic temporal engine reads T sequences per CTA (SpecLayout::qmajor)
+    const bool qmajor = sp.f64 && !warp_t && !long_t && ddmk::spatial_warp_f64_supported(W, H, sp.pixel_bytes) &&
                         std::getenv("DDM_B200_V1_SPATIAL") == nullptr;
+    const bool warp_s = ((warp_t || long_t) && ddmk::spatial_warp_supported(W, H, sp.pixel_bytes, sb) &&
+                         std::getenv("DDM_B200_V1_SPATIAL") == nullptr) || qmajor;
     ddmk::SpatialArgs sa = spatial_args(sp.d_frames, sp.pixel_bytes, W, H, N, sp.f64);
     sa.spec = d_spec;
     sa.slot_of_flat = d_slot;
@@ -488,9 +495,10 @@ uint64_t Engine::run(const RunSpec& sp, PhaseTimes* times) {
         lay.T = T;
         lay.g_begin = gb;
         lay.g_count = gc;
+        lay.qmajor = qmajor;
         // slots of a partial tile tail are never written by the spatial pass: zero them so
-        // the temporal kernel transforms zeros there
-        if (gc % T) {
+        // the temporal kernel transforms zeros there (q-major: the kernel zero-fills them)
+        if (gc % T && !qmajor) {
             const int64_t t0 = gc / T;
             check(cudaMemsetAsync(static_cast<char*>(d_spec) + (size_t)t0 * N * T * cs, 0,
                                   (size_t)N * T * cs, stream_), "tail memset");

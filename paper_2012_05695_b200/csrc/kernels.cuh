@@ -23,6 +23,9 @@ struct SpecLayout {
     int T = 4;
     int64_t g_begin = 0;   // first retained index of the group
     int64_t g_count = 0;   // slots in the group
+    // q-major spectra (spec[slot * N + n], what the register spatial kernels write) read by the
+    // generic temporal engine T sequences per CTA (f64 on register-friendly frame sizes)
+    bool qmajor = false;
     int64_t tiles() const { return (g_count + T - 1) / T; }
 };
 
@@ -156,6 +159,8 @@ cudaError_t launch_temporal_long(const TemporalArgs& a, int num_sms, void* out_q
 // Register-resident spatial kernels (spatial_warp.cu): f32, power-of-two W/2 and H in
 // [16, 1024], u16/u8 frames, wave-vector-major output (layout T = 1).
 bool spatial_warp_supported(int W, int H, int pixel_bytes, int scalar_bytes);
+// the same frame sizes with f64 arithmetic (launch_spatial_warp<double>; q-major output)
+bool spatial_warp_f64_supported(int W, int H, int pixel_bytes);
 
 // frames one column-pass CTA transforms together (the run length of its corner-turn stores)
 int spatial_warp_col_frames(int H);

@@ -373,5 +373,11 @@ cudaError_t launch_spatial_warp(const SpatialArgs& a, cudaStream_t stream, int p
 }
 
 template cudaError_t launch_spatial_warp<float>(const SpatialArgs&, cudaStream_t, int);
+template cudaError_t launch_spatial_warp<double>(const SpatialArgs&, cudaStream_t, int);
+
+bool spatial_warp_f64_supported(int W, int H, int pixel_bytes) {
+    // register budget of the f64 instantiations: rows up to W = 1024, columns up to H = 1024
+    return spatial_warp_supported(W, H, pixel_bytes, 4) && W <= 1024 && H <= 1024;
+}
 
 }  // namespace ddmk

@@ -41,10 +41,19 @@ __global__ void __launch_bounds__(256, 1) temporal_kernel(const cpx<S>* __restri
     const int nvalid = (int)(lay.g_count - s0 < T ? lay.g_count - s0 : T);
     const cpx<S>* src = spec + tile * (int64_t)N * T;
 
-    // 1. tile block [N][T] -> E[j][n] (coalesced: j fastest), zero padding beyond N
-    for (int idx = threadIdx.x; idx < N * T; idx += blockDim.x) {
-        const int n = idx / T, j = idx - n * T;
-        E[(size_t)j * N2 + n] = src[idx];
+    // 1. tile block [N][T] -> E[j][n] (coalesced: j fastest), zero padding beyond N; q-major
+    //    spectra: T contiguous sequences (coalesced along n), zeros past the group's end
+    if (lay.qmajor) {
+        const cpx<S>* qsrc = spec + s0 * (int64_t)N;
+        for (int idx = threadIdx.x; idx < N * T; idx += blockDim.x) {
+            const int j = idx / N, n = idx - j * N;
+            E[(size_t)j * N2 + n] = j < nvalid ? qsrc[idx] : cpx<S>{S(0), S(0)};
+        }
+    } else {
+        for (int idx = threadIdx.x; idx < N * T; idx += blockDim.x) {
+            const int n = idx / T, j = idx - n * T;
+            E[(size_t)j * N2 + n] = src[idx];
+        }
     }
     for (int idx = threadIdx.x; idx < T * (N2 - N); idx += blockDim.x) {
         const int j = idx / (N2 - N), n = N + idx - j * (N2 - N);
