@@ -417,7 +417,10 @@ uint64_t Engine::run(const RunSpec& sp, PhaseTimes* times) {
     const size_t cs = 2 * (size_t)sb;
     const bool warp_t = use_warp_temporal(N, (int)N2, sb);
     const bool long_t = !warp_t && use_long_temporal(N, (int)N2, sb);
-    const int T = (warp_t || long_t) ? 1 : ddmk::temporal_tile(N, (int)N2, sb);
+    // f64 at N2 = 2048: the f64 warp engine over q-major spectra (T = 1)
+    static const bool v1 = std::getenv("DDM_B200_V1") != nullptr;
+    const bool warp64 = sp.f64 && !v1 && ddmk::temporal_warp64_supported(N, (int)N2);
+    const int T = (warp_t || long_t || warp64) ? 1 : ddmk::temporal_tile(N, (int)N2, sb);
     if (T == 0)
         throw std::length_error("sequence of " + std::to_string(N) +
                                 " frames exceeds the single-CTA temporal engine (max " +
@@ -477,6 +480,10 @@ uint64_t Engine::run(const RunSpec& sp, PhaseTimes* times) {
     };
 
     last_engines_ = describe(warp_s, W, H, warp_t, long_t, N2, T, gmax, N, false);
+    if (warp64) {
+        const auto at = last_engines_.find("temporal=");
+        if (at != std::string::npos) last_engines_ = last_engines_.substr(0, at) + "temporal=warp64<1024>:map";
+    }
     // end-to-end streaming (RunSpec::frames_ready / host_out)
     frames_ready_ = sp.frames_ready.empty() ? nullptr : &sp.frames_ready;
     struct ResetFrames {
@@ -568,8 +575,9 @@ uint64_t Engine::run(const RunSpec& sp, PhaseTimes* times) {
             if (times) times->temporal_launches += chunks;
         } else {
             check(warp_t ? ddmk::launch_temporal_warp(ta, num_sms_, stream_)
-                         : sp.f64 ? ddmk::launch_temporal<double>(ta, stream_)
-                                  : ddmk::launch_temporal<float>(ta, stream_), "temporal kernel");
+                  : warp64 ? ddmk::launch_temporal_warp64(ta, num_sms_, stream_)
+                  : sp.f64 ? ddmk::launch_temporal<double>(ta, stream_)
+                           : ddmk::launch_temporal<float>(ta, stream_), "temporal kernel");
             if (times) times->temporal_launches += 1;
         }
         mark();

@@ -159,6 +159,10 @@ cudaError_t launch_temporal_long(const TemporalArgs& a, int num_sms, void* out_q
 // Register-resident spatial kernels (spatial_warp.cu): f32, power-of-two W/2 and H in
 // [16, 1024], u16/u8 frames, wave-vector-major output (layout T = 1).
 bool spatial_warp_supported(int W, int H, int pixel_bytes, int scalar_bytes);
+// f64 warp temporal engine (temporal_warp64.cu): N2 = 2048, q-major spectra, f64 map or
+// partial, no ring / diagnostics / segments
+bool temporal_warp64_supported(int N, int N2);
+cudaError_t launch_temporal_warp64(const TemporalArgs& a, int num_sms, cudaStream_t stream);
 // the same frame sizes with f64 arithmetic (launch_spatial_warp<double>; q-major output)
 bool spatial_warp_f64_supported(int W, int H, int pixel_bytes);
 
