@@ -14,6 +14,7 @@
 // The host runs them over chunks of frames sized so `mid` stays L2 resident.
 // Transform lengths in DDMK_LENGTH_CASES get compile-time pass plans; others take the
 // runtime radix-4/2/5/3 plan (or a direct DFT for other prime factors).
+#include <algorithm>
 #include <type_traits>
 
 #include "kernels.cuh"
@@ -98,32 +99,42 @@ loaded:
     }
 }
 
+// F frames x CB columns per CTA (CB adjacent columns of each frame are contiguous in `mid`):
+// the epilogue then writes each retained wave vector's F consecutive frames as one run
+// (F complex = 128 B at F = 16 in f32), instead of one 8-byte value per sequence per CTA
 template <typename S, int LC>
 __global__ void __launch_bounds__(kThreads)
-cols_kernel(const cpx<S>* __restrict__ mid, int H, int Wh, int CB, int N, int frame0,
+cols_kernel(const cpx<S>* __restrict__ mid, int H, int Wh, int CB, int F, int nframes, int N, int frame0,
             FftPlan plan, const cpx<S>* __restrict__ tw_col, cpx<S>* __restrict__ spec,
             SpecLayout lay, const int* __restrict__ slot_of_flat) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cpx<S>* buf = reinterpret_cast<cpx<S>*>(smem_raw);
     const int cblocks = (Wh + CB - 1) / CB;
-    const int fi = blockIdx.x / cblocks;
-    const int c0 = (blockIdx.x - fi * cblocks) * CB;
+    const int fb = blockIdx.x / cblocks;
+    const int c0 = (blockIdx.x - fb * cblocks) * CB;
     const int nc = min(CB, Wh - c0);
-    const cpx<S>* src = mid + ((size_t)fi * Wh + c0) * H;  // nc whole columns, contiguous
-    for (int idx = threadIdx.x; idx < nc * H; idx += blockDim.x) buf[idx] = src[idx];
+    const int f0 = fb * F;                      // within the chunk
+    const int nf = min(F, nframes - f0);
+    // buf[(fl * nc + cc) * H + r]: frame fl's columns are one contiguous run of nc * H
+    for (int idx = threadIdx.x; idx < nf * nc * H; idx += blockDim.x) {
+        const int fl = idx / (nc * H), rest = idx - fl * nc * H;
+        buf[idx] = mid[((size_t)(f0 + fl) * Wh + c0) * H + rest];
+    }
     __syncthreads();
-    batch_fft<-1, LC>(buf, H, nc, plan, tw_col, buf + CB * H);
+    batch_fft<-1, LC>(buf, H, nf * nc, plan, tw_col, buf + (size_t)F * CB * H);
 
-    const int n = frame0 + fi;
+    const int n0 = frame0 + f0;
     const int T = lay.T;
-    for (int idx = threadIdx.x; idx < nc * H; idx += blockDim.x) {
-        const int r = idx / nc, cc = idx - r * nc;
-        const int64_t f = (int64_t)r * Wh + c0 + cc;
-        const int64_t k = slot_of_flat ? (int64_t)slot_of_flat[f] : f;
-        const int64_t s = k - lay.g_begin;
-        if (k < 0 || s < 0 || s >= lay.g_count) continue;
-        const int64_t tile = s / T;
-        spec[(tile * N + n) * T + (s - tile * T)] = buf[cc * H + r];
+    // consecutive threads: consecutive frames of one wave vector
+    for (int idx = threadIdx.x; idx < nf * nc * H; idx += blockDim.x) {
+        const int fl = idx % nf, rc = idx / nf;
+        const int r = rc / nc, cc = rc - r * nc;
+        const int64_t fl_flat = (int64_t)r * Wh + c0 + cc;
+        const int64_t k = slot_of_flat ? (int64_t)slot_of_flat[fl_flat] : fl_flat;
+        const int64_t sl = k - lay.g_begin;
+        if (k < 0 || sl < 0 || sl >= lay.g_count) continue;
+        const int64_t tile = sl / T;
+        spec[(tile * N + n0 + fl) * T + (sl - tile * T)] = buf[(fl * nc + cc) * H + r];
     }
 }
 
@@ -150,12 +161,12 @@ void launch_rows(const SpatialArgs& a, int RB, const FftPlan& plan, size_t smem,
 }
 
 template <typename S, int LC>
-void launch_cols(const SpatialArgs& a, int CB, const FftPlan& plan, size_t smem, cudaStream_t st) {
+void launch_cols(const SpatialArgs& a, int CB, int F, const FftPlan& plan, size_t smem, cudaStream_t st) {
     auto k = cols_kernel<S, LC>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int Wh = a.W / 2 + 1;
-    const int grid = a.nframes * ((Wh + CB - 1) / CB);
-    k<<<grid, kThreads, smem, st>>>(static_cast<const cpx<S>*>(a.mid), a.H, Wh, CB, a.N,
+    const int grid = ((a.nframes + F - 1) / F) * ((Wh + CB - 1) / CB);
+    k<<<grid, kThreads, smem, st>>>(static_cast<const cpx<S>*>(a.mid), a.H, Wh, CB, F, a.nframes, a.N,
                                     a.frame0, plan, static_cast<const cpx<S>*>(a.tw_col.ptr),
                                     static_cast<cpx<S>*>(a.spec), a.layout, a.slot_of_flat);
 }
@@ -169,10 +180,13 @@ cudaError_t launch_spatial(const SpatialArgs& a, cudaStream_t stream) {
     const FftPlan pcol = make_rt_plan(Lc);
     const size_t cs = 2 * sizeof(S);
     const int RB = pick_rows(Lr, sizeof(S), prow.naive);
-    const int CB = pick_rows(Lc, sizeof(S), pcol.naive);
-    if (RB == 0 || CB == 0) return cudaErrorInvalidValue;
+    // column CTAs: F frames x CB columns, the same transform budget as a row CTA, frames first
+    const int CT = pick_rows(Lc, sizeof(S), pcol.naive);
+    if (RB == 0 || CT == 0) return cudaErrorInvalidValue;
+    const int F = std::min(CT, std::max(1, a.nframes));
+    const int CB = std::max(1, CT / F);
     const size_t smem_r = (size_t)RB * Lr * cs * (prow.naive ? 2 : 1);
-    const size_t smem_c = (size_t)CB * Lc * cs * (pcol.naive ? 2 : 1);
+    const size_t smem_c = (size_t)F * CB * Lc * cs * (pcol.naive ? 2 : 1);
 
 #define DDMK_ROWS_CASE(LEN)                                                             \
     case LEN:                                                                           \
@@ -194,10 +208,10 @@ cudaError_t launch_spatial(const SpatialArgs& a, cudaStream_t stream) {
     if (e != cudaSuccess) return e;
 
 #define DDMK_COLS_CASE(LEN) \
-    case LEN: launch_cols<S, LEN>(a, CB, pcol, smem_c, stream); break;
+    case LEN: launch_cols<S, LEN>(a, CB, F, pcol, smem_c, stream); break;
     switch (Lc) {
         DDMK_LENGTH_CASES(DDMK_COLS_CASE)
-    default: launch_cols<S, 0>(a, CB, pcol, smem_c, stream);
+    default: launch_cols<S, 0>(a, CB, F, pcol, smem_c, stream);
     }
 #undef DDMK_COLS_CASE
     return cudaGetLastError();
