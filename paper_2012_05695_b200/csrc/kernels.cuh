@@ -177,6 +177,6 @@ cudaError_t launch_spatial_warp(const SpatialArgs& a, cudaStream_t stream, int p
 // match it. Returns 0 when the sequence length is beyond what one CTA can hold.
 int temporal_tile(int N, int N2, int scalar_bytes);
 size_t temporal_smem_bytes(int N, int N2, int T, int scalar_bytes);
-int temporal_threads(int N2, int T);
+int temporal_threads(int N2, int T, int scalar_bytes);
 
 }  // namespace ddmk

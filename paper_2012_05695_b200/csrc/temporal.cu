@@ -22,8 +22,10 @@ namespace ddmk {
 
 namespace {
 
-template <typename S, typename OutT, int N2>
-__global__ void __launch_bounds__(256, 1) temporal_kernel(const cpx<S>* __restrict__ spec, int N, SpecLayout lay,
+// NT threads per CTA: 256, or 512 for long f64 transforms (T * N2 <= 8192 with one radix-16
+// butterfly per thread; more warps to hide the f64 shared-memory passes' latency)
+template <typename S, typename OutT, int N2, int NT>
+__global__ void __launch_bounds__(NT, 1) temporal_kernel(const cpx<S>* __restrict__ spec, int N, SpecLayout lay,
                                 const cpx<S>* __restrict__ tw,
                                 const cpx<S>* __restrict__ tw_half,
                                 const int* __restrict__ lag_index, OutT* __restrict__ out,
@@ -106,13 +108,14 @@ __global__ void __launch_bounds__(256, 1) temporal_kernel(const cpx<S>* __restri
     __syncthreads();
 
     // 3. forward transforms of all T sequences
-    smem_fft_ct<N2, 1, -1, (N2 > 8192 ? 4 : 2)>(E, N2, T, tw);
+    constexpr int kB16 = ((N2 > 8192 ? 4 : 2) * 256 / NT) > 0 ? ((N2 > 8192 ? 4 : 2) * 256 / NT) : 1;
+    smem_fft_ct<N2, 1, -1, kB16>(E, N2, T, tw);
 
     // 4. power spectrum folded for a half-length inverse: u[j] = P[2j] + i P[2j+1], P = |X|^2
     //    (read everything first, then overwrite the first half of each buffer in place)
     {
         constexpr int H2 = N2 / 2;
-        constexpr int MAXU = (N2 > 8192 ? 8192 : 4096) / 256 + 1;  // items per thread bound
+        constexpr int MAXU = (N2 > 8192 ? 8192 : 4096) / NT + 1;  // items per thread bound
         cpx<S> u[MAXU];
 #pragma unroll
         for (int it = 0; it < MAXU; ++it) {
@@ -137,7 +140,7 @@ __global__ void __launch_bounds__(256, 1) temporal_kernel(const cpx<S>* __restri
     }
 
     // 5. backward transforms of length N2/2 (sign +1)
-    if constexpr (N2 >= 2) smem_fft_ct<N2 / 2, 1, +1, (N2 > 8192 ? 4 : 2)>(E, N2, T, tw_half);
+    if constexpr (N2 >= 2) smem_fft_ct<N2 / 2, 1, +1, kB16>(E, N2, T, tw_half);
 
     // 6. real-input unfold: R(m) = E(m) + e^{+2 pi i m / N2} O(m) with
     //    E = (U[m] + conj U[N2/2 - m]) / 2, O = (U[m] - conj U[N2/2 - m]) / (2i);
@@ -183,7 +186,10 @@ size_t temporal_smem_bytes(int N, int N2, int T, int scalar_bytes) {
     return (size_t)T * N2 * 2 * scalar_bytes + (size_t)T * (N + 1) * 8 + (size_t)T * 16;
 }
 
-int temporal_threads(int, int) { return 256; }
+int temporal_threads(int N2, int T, int scalar_bytes) {
+    static const bool t256 = std::getenv("DDM_GENERIC_T256") != nullptr;
+    return (!t256 && scalar_bytes == 8 && N2 >= 4096 && (size_t)T * N2 <= 8192) ? 512 : 256;
+}
 
 // Sequences per tile. Capacity: 256 threads x 2 radix-16 butterflies -> T * N2 <= 8192
 // (N2 = 16384 runs alone with 4 butterflies per thread). Prefer the largest T <= 8 whose
@@ -255,8 +261,8 @@ template <typename S, typename OutT, int N2>
 void launch_t(const TemporalArgs& a, cudaStream_t stream) {
     const int T = a.layout.T;
     const size_t smem = temporal_smem_bytes(a.N, N2, T, sizeof(S));
-    const int threads = temporal_threads(N2, T);
-    auto k = temporal_kernel<S, OutT, N2>;
+    const int threads = temporal_threads(N2, T, sizeof(S));
+    auto k = threads == 512 ? temporal_kernel<S, OutT, N2, 512> : temporal_kernel<S, OutT, N2, 256>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k<<<(unsigned)a.layout.tiles(), threads, smem, stream>>>(
         static_cast<const cpx<S>*>(a.spec), a.N, a.layout, static_cast<const cpx<S>*>(a.tw.ptr),
