@@ -12,11 +12,14 @@ LIB_DIR = ROOT / "paper_2012_05695_b200"
 
 
 def _build_and_run(tmp_path, name):
-    cxx = shutil.which("g++") or shutil.which("c++")
+    c_src = (ROOT / "tests" / "cpp" / f"{name}.c").exists()
+    cxx = (shutil.which("gcc") or shutil.which("cc")) if c_src else (shutil.which("g++") or shutil.which("c++"))
     if cxx is None or not (LIB_DIR / "libddm_b200.so").exists():
-        pytest.skip("no C++ compiler or library not built")
+        pytest.skip("no C/C++ compiler or library not built")
     exe = tmp_path / name
-    subprocess.run([cxx, "-std=c++20", "-O1", f"-I{ROOT / 'include'}", str(ROOT / "tests" / "cpp" / f"{name}.cpp"),
+    std = "-std=c11" if c_src else "-std=c++20"
+    src = ROOT / "tests" / "cpp" / (f"{name}.c" if c_src else f"{name}.cpp")
+    subprocess.run([cxx, std, "-O1", f"-I{ROOT / 'include'}", str(src),
                     f"-L{LIB_DIR}", "-lddm_b200", f"-Wl,-rpath,{LIB_DIR}", "-o", str(exe)],
                    check=True, capture_output=True, text=True, timeout=300)
     r = subprocess.run([str(exe), str(tmp_path / "work")], capture_output=True, text=True, timeout=120)
@@ -27,6 +30,12 @@ def _build_and_run(tmp_path, name):
 @pytest.mark.parametrize("name", ["archive_api", "analysis_api"])
 def test_cpp_driver(tmp_path, name):
     _build_and_run(tmp_path, name)
+
+
+@pytest.mark.gpu
+def test_c_session_api_on_device(tmp_path):
+    """A plain C program drives the staging session through include/ddm_b200.h on the B200."""
+    _build_and_run(tmp_path, "session_api")
 
 
 @pytest.mark.gpu
