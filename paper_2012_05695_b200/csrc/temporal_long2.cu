@@ -215,22 +215,31 @@ temporal_long2_kernel(const cpx<float>* __restrict__ spec, const __grid_constant
 #pragma unroll 1
         for (int half = 0; half < 2; ++half) {
             const int r = w + G * half;
-            cpx<float> wj[H];
-#pragma unroll
-            for (int j = 0; j < H; ++j) wj[j] = wj_tab[r * H + j];
+            // sum_j t[n1 + 1024 j] W_R^{j r}: W_4^r = (-i)^r is a swap and two signs (warp-
+            // uniform), so R = 4 needs no complex product and R = 8 one:
+            // (t0 + W_4^r t2) + W_8^r (t1 + W_4^r t3)
+            const bool sw = r & 1;
+            const float sa = (r & 2) ? -1.f : 1.f, sb = ((r + 1) & 2) ? -1.f : 1.f;
+            auto rot_add = [&](cpx<float> base, cpx<float> t) {   // base + W_4^r t
+                return cpx<float>{fmaf(sa, sw ? t.y : t.x, base.x), fmaf(sb, sw ? t.x : t.y, base.y)};
+            };
+            const cpx<float> w8 = wj_tab[r * H + (H > 1 ? 1 : 0)];
             const cpx<float> tl = tw_lane[r * 32 + lane];
+            auto tap = [&](int n) -> cpx<float> {
+                return (FULL || n < N) ? stage[n] : cpx<float>{0.f, 0.f};
+            };
             cpx<float> v[32];
 #pragma unroll
             for (int b = 0; b < 32; ++b) {
                 const int n1 = lane + 32 * b;
-                cpx<float> a = {0.f, 0.f};
-#pragma unroll
-                for (int j = 0; j < H; ++j) {
-                    const int n = n1 + kF2 * j;
-                    if (FULL || n < N) {
-                        const cpx<float> t = stage[n];
-                        a = (j == 0) ? t : cadd(a, cmul(t, wj[j]));
-                    }
+                cpx<float> a;
+                if constexpr (H == 2) {
+                    a = rot_add(tap(n1), tap(n1 + kF2));
+                } else {
+                    static_assert(H == 4, "R = 4 or 8");
+                    const cpx<float> A = rot_add(tap(n1), tap(n1 + 2 * kF2));
+                    const cpx<float> B = rot_add(tap(n1 + kF2), tap(n1 + 3 * kF2));
+                    a = cfma(w8, B, A);
                 }
                 v[b] = cmul(cmul(a, tl), tw_pre[r * 32 + b]);
             }
