@@ -330,8 +330,12 @@ void Engine::spatial_pass(ddmk::SpatialArgs sa, bool f64, bool warp_s, PhaseTime
     // tail overhead per chunk outweighs L2 residency, so the register path takes two chunks
     // (row pass of one overlapping the column pass of the other) up to 1 GiB per buffer.
     static const char* mid_env = std::getenv("DDM_MID_MB");
+    // Frames of >= 8 MB per row-pass output (2048^2) go in chunks of <= 560 MB: C4 spatial
+    // 73 -> 70 ms against 1 GiB chunks (32 vs 56 frames; 16 frames 72 ms, 40 frames 74 ms); C2
+    // and C3 are fastest with the two large chunks (r02 sweep)
+    const size_t warp_cap = per_frame >= (size_t(8) << 20) ? size_t(560) << 20 : size_t(1) << 30;
     const size_t mid_budget = mid_env ? (size_t)std::max(1, std::atoi(mid_env)) << 20
-                            : warp_s  ? std::min<size_t>((size_t)(N + 1) / 2 * per_frame, size_t(1) << 30)
+                            : warp_s  ? std::min<size_t>((size_t)(N + 1) / 2 * per_frame, warp_cap)
                                       : size_t(48) << 20;
     int F = (int)std::max<int64_t>(1, std::min<int64_t>(N, mid_budget / per_frame));
     if (warp_s) {
