@@ -92,8 +92,10 @@ bool temporal_long_supported(int N, int N2, int scalar_bytes) {
 }
 
 int64_t temporal_long_chunk(int N) {
-    // q-major staging block of the map mode: ~1 GiB of f32
-    return std::max<int64_t>(1, (int64_t)(1u << 28) / N);
+    // q-major staging block of the map mode: ~1 GiB of f32 (DDM_LONG_CHUNK_MB overrides)
+    static const char* env = std::getenv("DDM_LONG_CHUNK_MB");
+    const int64_t bytes = env ? (int64_t)std::max(1, std::atoi(env)) << 20 : (int64_t)1 << 30;
+    return std::max<int64_t>(1, bytes / 4 / N);
 }
 
 cudaError_t launch_temporal_long(const TemporalArgs& a, int num_sms, void* out_q,
