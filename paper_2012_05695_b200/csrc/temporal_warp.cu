@@ -227,7 +227,7 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
 
         // ---- S(m) = sum_{n >= m} (p_n + p_{N-1-n}) = (N - m) d_a(m)  (`temporal.cpp:19-42`):
         //      lane a scans n = 32 a + j in f32, lane totals are suffix-summed in f64
-        float sv[32];
+        float* sarea = sw;  // S(m) replaces |t|^2
         {
             float qv[32];
 #pragma unroll
@@ -252,28 +252,35 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
             }
             const float base = (float)(incl - (double)r);
             __syncwarp();
-            float* sarea = sw;  // S(m) replaces |t|^2
 #pragma unroll
             for (int j = 0; j < 32; ++j) sarea[padded(32 * lane + j)] = qv[j] + base;
             __syncwarp();
-#pragma unroll
-            for (int d = 0; d < 32; ++d) sv[d] = sarea[padded(lane + 32 * d)];
-            __syncwarp();
         }
 
-        // ---- unfold + combine on the lane's own m = c + 32 d; U[L - m] sits in lane
-        //      (32 - c) mod 32, register 31 - d (lane 0: its own register (32 - d) mod 32)
-        //      2 Re R(m) = (A.x + B.x) + w.x (A.y + B.y) + w.y (A.x - B.x), w = W_N2^{-m}
-        //      d(m) = (S(m) - 2 corr(m)) / (N - m), 2 corr(m) = 2 Re R(m) / N2
+        // ---- unfold + combine, two lags per step: for m = c + 32 d (d < 16), U[L - m] sits in
+        //      lane (32 - c) mod 32, register 31 - d (lane 0: its own register (32 - d) mod 32), and
+        //      with S1 = A.x + B.x, P = w.x (A.y + B.y) + w.y (A.x - B.x), w = W_N2^{-m}:
+        //      2 Re R(m) = S1 + P and 2 Re R(L - m) = S1 - P (w(L - m) = -conj w(m), A and B
+        //      swap). L - m = (32 - c) + 32 (31 - d) is the mirrored lane's upper half (lane 0:
+        //      its own, lag 512 separately), so every lag is produced once; S(m) and 1/(N - m)
+        //      come from shared memory. d(m) = (S(m) - 2 corr(m)) / (N - m), 2 corr = 2 Re R / N2.
         const int src = (32 - lane) & 31;
-        // opaque per-sequence copy of the lane base: stops the compiler from hoisting the 32
-        // products base * W_N2^{-32 d} out of the sequence loop (64 registers)
+        // opaque per-sequence copy of the lane base: stops the compiler from hoisting the 16
+        // products base * W_N2^{-32 d} out of the sequence loop
         cpx<float> bu;
         asm volatile("mov.b32 %0, %1;" : "=f"(bu.x) : "f"(base_unf.x));
         asm volatile("mov.b32 %0, %1;" : "=f"(bu.y) : "f"(base_unf.y));
         constexpr float inv_n2 = 1.0f / (float)kN2;
+        auto finish = [&](int m, float re2) {
+            if (m < N) {
+                const float val = fmaf(-re2, inv_n2, sarea[padded(m)]) * rcp[m];
+                emit(m, (m == 0) ? 0.f : val);
+                if constexpr (kDiag)
+                    if (corr_out && live) corr_out[q * N + m] = 0.5 * (double)re2 / (double)kN2;
+            }
+        };
 #pragma unroll
-        for (int d = 0; d < 32; ++d) {
+        for (int d = 0; d < 16; ++d) {
             const int m = lane + 32 * d;
             cpx<float> Bc;
             Bc.x = __shfl_sync(0xffffffffu, v[31 - d].x, src);
@@ -281,13 +288,15 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
             if (lane == 0) Bc = v[(32 - d) & 31];
             const cpx<float> A = v[d];
             const cpx<float> w = cmul(bu, ct_w<+1, float>(32 * d, kN2));  // exp(+2 pi i m / N2)
-            const float re2 = (A.x + Bc.x) + (w.x * (A.y + Bc.y) + w.y * (A.x - Bc.x));
-            if (m < N) {
-                const float val = fmaf(-re2, inv_n2, sv[d]) * rcp[m];
-                emit(m, (m == 0) ? 0.f : val);
-                if constexpr (kDiag)
-                    if (corr_out && live) corr_out[q * N + m] = 0.5 * (double)re2 / (double)kN2;
-            }
+            const float S1 = A.x + Bc.x;
+            const float P = w.x * (A.y + Bc.y) + w.y * (A.x - Bc.x);
+            finish(m, S1 + P);
+            finish(kL - m, S1 - P);   // kL - m = kL (d = 0, lane 0) is never < N
+        }
+        if (lane == 0) {   // lag 512 = L / 2, its own mirror: U[512] in register 16
+            const cpx<float> A = v[16];
+            const cpx<float> w = ct_w<+1, float>(512, kN2);
+            finish(512, (A.x + A.x) + (w.x * (A.y + A.y)));
         }
         if (kDiag && mean_out && live && lane == 0) {
             mean_out[2 * q] = (double)mx;
