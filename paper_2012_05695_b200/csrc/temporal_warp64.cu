@@ -157,8 +157,9 @@ temporal_warp64_kernel(const cpx<double>* __restrict__ spec, int N_rt, int64_t n
             cpx<double> bu;
             asm volatile("mov.b64 %0, %1;" : "=d"(bu.x) : "d"(base_unf.x));
             asm volatile("mov.b64 %0, %1;" : "=d"(bu.y) : "d"(base_unf.y));
+            // two lags per step: 2 Re r(m) = S1 + P, 2 Re r(L - m) = S1 - P (temporal_warp.cu)
 #pragma unroll
-            for (int d = 0; d < 32; ++d) {
+            for (int d = 0; d < 16; ++d) {
                 const int m = lane + 32 * d;
                 cpx<double> B;
                 B.x = __shfl_sync(0xffffffffu, v[31 - d].x, src);
@@ -166,7 +167,15 @@ temporal_warp64_kernel(const cpx<double>* __restrict__ spec, int N_rt, int64_t n
                 if (lane == 0) B = v[(32 - d) & 31];
                 const cpx<double> A = v[d];
                 const cpx<double> w = cmul(bu, ct_w<+1, double>(32 * d, kN2));
-                my.w[padded(m)] = (A.x + B.x) + (w.x * (A.y + B.y) + w.y * (A.x - B.x));
+                const double S1 = A.x + B.x;
+                const double P = w.x * (A.y + B.y) + w.y * (A.x - B.x);
+                my.w[padded(m)] = S1 + P;
+                if (kL - m < kL) my.w[padded(kL - m)] = S1 - P;
+            }
+            if (lane == 0) {   // lag 512, its own mirror
+                const cpx<double> A = v[16];
+                const cpx<double> w = ct_w<+1, double>(512, kN2);
+                my.w[padded(512)] = (A.x + A.x) + w.x * (A.y + A.y);
             }
         }
         // |t|^2 (f64, `temporal.cpp:25-30`) of the shifted sequence into the exchange area
