@@ -949,6 +949,13 @@ void Engine::spectra(const void* d_frames, int pixel_bytes, int W, int H, int N,
     check(cudaStreamSynchronize(stream_), "sync");
 }
 
+void Engine::transform1d(void* d_data, int len, bool f64, int sign) {
+    check(cudaSetDevice(device_), "cudaSetDevice");
+    void* scratch = buffer("fft1d", (size_t)len * (f64 ? 16 : 8));
+    check(ddmk::launch_fft1d(d_data, scratch, len, f64, sign, twiddles(len, f64), stream_), "fft1d kernels");
+    check(cudaStreamSynchronize(stream_), "sync");
+}
+
 void Engine::sequences(const void* d_seq, int64_t q, int64_t n, bool f64, double* d_out,
                        double* d_a_out, double* corr_out) {
     check(cudaSetDevice(device_), "cudaSetDevice");

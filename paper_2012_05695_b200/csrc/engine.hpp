@@ -134,6 +134,10 @@ public:
     void spectra(const void* d_frames, int pixel_bytes, int W, int H, int N, bool f64,
                  void* d_out);
 
+    // One unnormalised complex 1D transform of d_data (len complex, working precision) in
+    // place on the engine stream, sign -1 forward / +1 backward (`ddm::TemporalTransform`).
+    void transform1d(void* d_data, int len, bool f64, int sign);
+
     // Sharded WITH_FT, step 1 on one rank: the rank's frame shard
     // d_frames [n][H][W] -> d_spec [H*(W/2+1)][n] (every wave vector, q-major, working
     // precision). Consecutive wave-vector ranges of d_spec are the all-to-all send blocks.

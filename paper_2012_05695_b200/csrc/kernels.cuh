@@ -179,4 +179,9 @@ int temporal_tile(int N, int N2, int scalar_bytes);
 size_t temporal_smem_bytes(int N, int N2, int T, int scalar_bytes);
 int temporal_threads(int N2, int T, int scalar_bytes);
 
+// One unnormalised complex transform of `len` points in place (fft1d.cu; sign -1 forward,
+// +1 backward); scratch holds len complex, tw = exp(-2 pi i j / len) in the same precision.
+cudaError_t launch_fft1d(void* data, void* scratch, int len, bool f64, int sign, const void* tw,
+                         cudaStream_t stream);
+
 }  // namespace ddmk

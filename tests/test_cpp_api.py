@@ -27,7 +27,7 @@ def _build_and_run(tmp_path, name):
     assert r.stdout.strip().startswith("OK")
 
 
-@pytest.mark.parametrize("name", ["archive_api", "analysis_api"])
+@pytest.mark.parametrize("name", ["archive_api", "analysis_api", "header_api"])
 def test_cpp_driver(tmp_path, name):
     _build_and_run(tmp_path, name)
 
@@ -43,3 +43,11 @@ def test_cpp_run_api_on_device(tmp_path):
     """INTEGRATION.md §1: a C++ program compiled against include/ddm/*.hpp runs ddm::run,
     ddm::compare and ddm::analyze on the B200 through libddm_b200.so."""
     _build_and_run(tmp_path, "run_api")
+
+
+@pytest.mark.gpu
+def test_cpp_transform_objects_on_device(tmp_path):
+    """ddm::SpatialTransform / ddm::TemporalTransform (include/ddm/fft.hpp, the reference's
+    `fft.hpp` seams) on the B200 against a direct long-double DFT: f32 within 2e-6 / 3e-6 and
+    f64 within 1e-13 of the largest output magnitude, odd and prime lengths included."""
+    _build_and_run(tmp_path, "fft_api")
