@@ -9,6 +9,6 @@ for r in $(seq $rounds); do
   for v in "$a" "$b"; do
     env $v timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/e2e_${tag}.log 2>&1
     echo -n "$v: "
-    grep '^{' gpurun_out/e2e_${tag}.log | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); e=d['e2e']; print(round(d['ms_per_step'],3), round(e['ms_per_step'],2), {k: round(v*1e3,2) for k,v in e['phases_s'].items()})"
+    grep '^{' gpurun_out/e2e_${tag}.log | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); e=d['e2e'].get('serial', d['e2e']); print(round(d['ms_per_step'],3), round(e['ms_per_step'],2), {k: round(v*1e3,2) for k,v in e['phases_s'].items()})"
   done
 done

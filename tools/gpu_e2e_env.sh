@@ -10,7 +10,7 @@ for cfg in "$@"; do
 import json, sys
 try:
     d = json.loads(open("gpurun_out/e2e_ab.json").read().strip().splitlines()[-1])
-    e = d["e2e"]
+    e = d["e2e"].get("serial", d["e2e"])
     print("%-28s e2e %.2f ms  %s" % (sys.argv[1], e["ms_per_step"], {k: round(v * 1e3, 2) for k, v in e["phases_s"].items()}))
 except Exception as ex:
     print(sys.argv[1], "FAILED", ex, open("gpurun_out/e2e_ab.err").read()[-600:])

@@ -12,6 +12,6 @@ import json
 d = json.loads(open("gpurun_out/quick_bench.json").read().strip().splitlines()[-1])
 st = d["stages"]
 print("value %.0f ms/step %.4f spatial %.4f temporal %.4f" % (d["value"], d["ms_per_step"], st["spatial_ms"], st["temporal_ms"]))
-e = d["e2e"]
+e = d["e2e"].get("serial", d["e2e"])
 print("e2e %.0f frames/s, %.2f ms; phases %s" % (e["value"], e["ms_per_step"], {k: round(v * 1e3, 3) for k, v in e["phases_s"].items()}))
 PY
