@@ -130,7 +130,9 @@ __global__ void restore_kernel(const cpx<S>* __restrict__ seq, int64_t q, int n,
 std::string describe(bool warp_s, int W, int H, bool warp_t, bool long_t, int64_t N2, int T,
                      int64_t n_q, int N, bool ring) {
     std::string s = "spatial=";
-    s += warp_s ? "rows2<" + std::to_string(W / 2) + ">+cols2<" + std::to_string(H) + ">" : "generic";
+    s += warp_s ? "rows2<" + std::to_string(W / 2) + ">+cols2<" + std::to_string(H) + ">" +
+                      (H == 2048 && ddmk::spatial_cols_pair() ? ":pair" : "")
+                : "generic";
     s += " temporal=";
     if (warp_t) {
         s += "warp<1024>";

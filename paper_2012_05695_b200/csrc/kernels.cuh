@@ -166,6 +166,8 @@ cudaError_t launch_temporal_warp64(const TemporalArgs& a, int num_sms, cudaStrea
 // the same frame sizes with f64 arithmetic (launch_spatial_warp<double>; q-major output)
 bool spatial_warp_f64_supported(int W, int H, int pixel_bytes);
 
+// H = 2048 f32 column pass with two warps per column (spatial_warp.cu; DDM_COLS2_PAIR=0 off)
+bool spatial_cols_pair();
 // frames one column-pass CTA transforms together (the run length of its corner-turn stores)
 int spatial_warp_col_frames(int H);
 // parts: 1 = row pass (frames -> mid), 2 = column pass (mid -> spectra), 3 = both

@@ -144,19 +144,17 @@ __device__ __forceinline__ cpx<S> ld_cg(const cpx<S>* p) {
 // Column-pass epilogue: the CTA's transposed stage sm[r * (F + 1) + f] (wave-vector row r,
 // frame f of this CTA's nf frames starting at n0, column c) -> the spectra, a peer's receive
 // buffer, or a cutoff / group subset.
-template <typename S, int HL>
+template <typename S, int HL, int F = kThreads / split_a<HL>(), int NT = kThreads>
 __device__ __forceinline__ void cols_epilogue(const cpx<S>* sm, int Wh, int N, int n0, int nf, int c,
                                               cpx<S>* __restrict__ spec, const SpecLayout& lay,
                                               const int* __restrict__ slot_of_flat,
                                               const PeerTable& peers) {
-    constexpr int A = split_a<HL>();
-    constexpr int F = kThreads / A;
     constexpr int SP = F + 1;
     const int64_t plane = (int64_t)HL * Wh;
     if (peers.ranks > 0) {
         // fused corner turn: every wave vector goes to its owner's receive buffer (a peer
         // pointer over NVLink); rows ascend with j, so the owner index only moves forward
-        constexpr int RS = kThreads / F;
+        constexpr int RS = NT / F;
         const int f = threadIdx.x % F, rb = threadIdx.x / F;
         if (f < nf) {
             const int64_t kstep = (int64_t)RS * Wh;
@@ -176,10 +174,35 @@ __device__ __forceinline__ void cols_epilogue(const cpx<S>* sm, int Wh, int N, i
         }
         return;
     }
+    if constexpr (sizeof(S) == 4) {
+    if (!slot_of_flat && lay.g_begin == 0 && lay.g_count == plane && ((N | n0) & 1) == 0) {
+        // every wave vector of the plane, identity slots, f32: thread (fp, rb + RS j) copies
+        // frames fp, fp + 1 of wave vector (r, c) as one 16-byte store; TPR consecutive
+        // threads fill an F-frame run
+        constexpr int TPR = F / 2, RS = NT / TPR;
+        const int fp = 2 * (threadIdx.x % TPR), rb = threadIdx.x / TPR;
+        if (fp < nf) {
+            cpx<S>* dst = spec + ((int64_t)rb * Wh + c) * N + n0 + fp;
+            const int64_t step = (int64_t)RS * Wh * N;
+            const bool pair = fp + 1 < nf;
+#pragma unroll 8
+            for (int j = 0; j < HL / RS; ++j) {
+                const cpx<S>* src = sm + (rb + RS * j) * SP + fp;
+                if (pair) {
+                    const cpx<S> u = src[0], w = src[1];
+                    __stcs(reinterpret_cast<float4*>(dst + j * step), make_float4(u.x, u.y, w.x, w.y));
+                } else {
+                    st_stream(dst + j * step, src[0]);
+                }
+            }
+        }
+        return;
+    }
+    }
     if (!slot_of_flat && lay.g_begin == 0 && lay.g_count == plane) {
         // every wave vector of the plane, identity slots: thread (f, rb + RS j) copies one
         // frame of wave vector (r, c); consecutive threads fill F-frame runs
-        constexpr int RS = kThreads / F;             // row stride
+        constexpr int RS = NT / F;                   // row stride
         const int f = threadIdx.x % F, rb = threadIdx.x / F;
         if (f < nf) {
             cpx<S>* dst = spec + ((int64_t)rb * Wh + c) * N + n0 + f;
@@ -189,7 +212,7 @@ __device__ __forceinline__ void cols_epilogue(const cpx<S>* sm, int Wh, int N, i
         }
         return;
     }
-    for (int idx = threadIdx.x; idx < HL * F; idx += kThreads) {
+    for (int idx = threadIdx.x; idx < HL * F; idx += NT) {
         const int r = idx / F, f = idx - r * F;
         if (f >= nf) continue;
         const int64_t flat = (int64_t)r * Wh + c;
@@ -273,6 +296,106 @@ cols2_kernel(const cpx<S>* __restrict__ mid, int Wh, int N, int frame0, int nfra
                              blockIdx.x, smem_raw);
 }
 
+// ---------------------------------------------------------------------------- cols, H = 2048
+// The 2048-point column pass with two warps per column (cols2<2048>:pair). With one warp per
+// column a lane holds 64 values (187 registers, one 8-warp CTA per SM: latency-bound, 52% of
+// HBM at C4). Here lane a < 64 of a column group holds x[a + 64 b], b < 32:
+//   Y[a][k1]  = W_2048^{a k1} sum_b x[a + 64 b] W_32^{b k1}                 (DFT_32 in registers)
+//   lane (k1, a1), a1 = a & 1, reads Y[2 a2 + a1][k1] through shared memory (pitch 66: the
+//   half-warp's 16 loads hit 16 distinct bank pairs) and forms
+//   Z_a1[k] = sum_a2 Y[2 a2 + a1][k1] W_32^{a2 k}                            (DFT_32)
+//   X[k1 + 32 k]        = Z_0[k] + W_64^k Z_1[k]
+//   X[k1 + 32 (k + 32)] = Z_0[k] - W_64^k Z_1[k]                            (lane-pair radix 2)
+// 32 values per lane (~110 registers), 16 warps per SM; 8 frames per CTA as before, so the
+// corner-turn runs stay 64 bytes.
+constexpr int kPairThreads = 512;
+constexpr int kPairF = kPairThreads / 64;   // frames per CTA
+constexpr int kPairP = 66;                  // exchange pitch (complex)
+
+template <typename S>
+__global__ void __launch_bounds__(kPairThreads, 1)
+cols2_pair_kernel(const cpx<S>* __restrict__ mid, int Wh, int N, int frame0, int nframes,
+                  const cpx<S>* __restrict__ tw_col, cpx<S>* __restrict__ spec, SpecLayout lay,
+                  const int* __restrict__ slot_of_flat, const __grid_constant__ PeerTable peers) {
+    constexpr int HL = 2048, B = 32, F = kPairF, P = kPairP, SP = F + 1;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cpx<S>* sm = reinterpret_cast<cpx<S>*>(smem_raw);
+    const int g = threadIdx.x >> 6, a = threadIdx.x & 63;
+    const int fblocks = (nframes + F - 1) / F;
+    const int c = blockIdx.x / fblocks;
+    const int f0 = (blockIdx.x - c * fblocks) * F;
+    const int nf = min(F, nframes - f0);
+    const bool act = g < nf;
+    const int k1 = a >> 1, a1 = a & 1;
+
+    cpx<S> v[B];
+    if (act) {
+        LaneTw<B, S> tw;
+        tw.init_from(tw_col, a, HL);
+        const cpx<S>* col = mid + ((size_t)(f0 + g) * Wh + c) * HL;
+#pragma unroll
+        for (int b = 0; b < B; ++b) v[b] = ld_cg(col + a + 64 * b);
+        RegDft<B, -1, S>::run(v);
+#pragma unroll
+        for (int k = 1; k < B; ++k) v[k] = cmul(v[k], tw.template get<-1>(k));
+        cpx<S>* ex = sm + g * B * P;
+#pragma unroll
+        for (int k = 0; k < B; ++k) ex[k * P + a] = v[k];
+        {
+            // the row-pass buffer has been consumed: drop its L2 lines without write-back
+            const char* base = reinterpret_cast<const char*>(col);
+            for (int l = a; l < HL * (int)sizeof(cpx<S>) / 128; l += 64)
+                asm volatile("discard.global.L2 [%0], 128;" ::"l"(base + 128 * l) : "memory");
+        }
+        asm volatile("bar.sync %0, 64;" ::"r"(1 + g) : "memory");   // this column group only
+#pragma unroll
+        for (int a2 = 0; a2 < B; ++a2) v[a2] = ex[k1 * P + 2 * a2 + a1];
+        RegDft<B, -1, S>::run(v);
+        // odd lanes: W_64^k Z_1[k] (compile-time constants, selected per lane)
+        const S one = a1 ? S(0) : S(1), sel = a1 ? S(1) : S(0);
+#pragma unroll
+        for (int k = 1; k < B; ++k) {
+            const cpx<S> w = ct_w<-1, S>(k, 64);
+            v[k] = cmul(v[k], cpx<S>{one + sel * w.x, sel * w.y});
+        }
+        // pair butterfly: even lane Z0 + t, odd lane Z0 - t (t = its own value)
+        const S sgn = a1 ? S(-1) : S(1);
+#pragma unroll
+        for (int k = 0; k < B; ++k) {
+            const S px = __shfl_xor_sync(0xffffffffu, v[k].x, 1);
+            const S py = __shfl_xor_sync(0xffffffffu, v[k].y, 1);
+            v[k] = {fma(sgn, v[k].x, px), fma(sgn, v[k].y, py)};
+        }
+    }
+    __syncthreads();  // every group's exchange reads are done: the area becomes the stage
+    if (act) {
+#pragma unroll
+        for (int k = 0; k < B; ++k) sm[(k1 + 32 * (k + 32 * a1)) * SP + g] = v[k];
+    }
+    __syncthreads();
+    cols_epilogue<S, HL, F, kPairThreads>(sm, Wh, N, frame0 + f0, nf, c, spec, lay, slot_of_flat, peers);
+}
+
+constexpr size_t pair_smem(size_t cs) {
+    const size_t ex = (size_t)kPairF * 32 * kPairP, st = (size_t)2048 * (kPairF + 1);
+    return (ex > st ? ex : st) * cs;
+}
+
+template <typename S>
+cudaError_t launch_cols2_pair(const SpatialArgs& a, cudaStream_t st) {
+    auto k = cols2_pair_kernel<S>;
+    const size_t smem = pair_smem(sizeof(cpx<S>));
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const int Wh = a.W / 2 + 1;
+    const int grid = Wh * ((a.nframes + kPairF - 1) / kPairF);
+    k<<<grid, kPairThreads, smem, st>>>(static_cast<const cpx<S>*>(a.mid), Wh, a.N, a.frame0,
+                                        a.nframes, static_cast<const cpx<S>*>(a.tw_col.ptr),
+                                        static_cast<cpx<S>*>(a.spec), a.layout, a.slot_of_flat,
+                                        a.peers);
+    return cudaGetLastError();
+}
+
 // complex slots of the column pass's exchange / transpose area
 template <int HL>
 __host__ __device__ constexpr int cols_area() {
@@ -338,6 +461,15 @@ bool spatial_warp_supported(int W, int H, int pixel_bytes, int scalar_bytes) {
     return H % (kThreads / A) == 0;  // whole row blocks per CTA
 }
 
+bool spatial_cols_pair() {
+    // DDM_COLS2_PAIR=0: the one-warp 2048-point column pass (A/B)
+    static const bool on = [] {
+        const char* e = std::getenv("DDM_COLS2_PAIR");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 int spatial_warp_col_frames(int H) {
     const int e = 31 - __builtin_clz(H);
     return kThreads / std::min(1 << (e / 2), 32);
@@ -361,6 +493,9 @@ cudaError_t launch_spatial_warp(const SpatialArgs& a, cudaStream_t stream, int p
     if (e != cudaSuccess) return e;
     }
     if (!(parts & 2)) return cudaSuccess;
+    if constexpr (std::is_same_v<S, float>) {
+        if (a.H == 2048 && spatial_cols_pair()) return launch_cols2_pair<S>(a, stream);
+    }
 #define DDMK_C2(LEN) \
     case LEN: e = launch_cols2<S, LEN>(a, stream); break;
     switch (a.H) {
