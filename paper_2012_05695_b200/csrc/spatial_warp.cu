@@ -91,25 +91,38 @@ __device__ __forceinline__ void rows2_body(const Pix* __restrict__ frames, int H
     __syncthreads();
 
     // even/odd split: X[c] = (Z[c] + conj Z[L-c]) / 2 + W_W^c (Z[c] - conj Z[L-c]) / (2i)
-    // thread (rr, cb) owns row rr and the columns c = cb + CS j: fixed strides, no division,
-    // all twiddle loads hoisted by the unrolled loop
-    constexpr int CS = kThreads / RB;                // column stride
+    // thread (rp, cb) owns rows 2 rp, 2 rp + 1 and the columns c = cb + CS j: fixed strides,
+    // no division, one twiddle load per column for both rows, and the two rows' values of a
+    // column (adjacent in mid[f][col][row]) leave as one 16-byte store (f32)
+    constexpr int RP = RB / 2;                       // row pairs
+    constexpr int CS = kThreads / RP;                // column stride
     constexpr int NJ = (Wh + CS - 1) / CS;
     const S half = S(0.5);
-    const int rr = threadIdx.x % RB, cb = threadIdx.x / RB;
-    const cpx<S>* z = region_base + rr * REG;
-    cpx<S>* dst = mid + (size_t)fi * Wh * H + r0 + rr + (size_t)cb * H;
+    const int rp = threadIdx.x % RP, cb = threadIdx.x / RP;
+    const cpx<S>* z0 = region_base + (2 * rp) * REG;
+    const cpx<S>* z1 = z0 + REG;
+    cpx<S>* dst = mid + (size_t)fi * Wh * H + r0 + 2 * rp + (size_t)cb * H;
     const size_t step = (size_t)CS * H;
-#pragma unroll
-    for (int j = 0; j < NJ; ++j) {
-        const int c = cb + CS * j;
-        if (j == NJ - 1 && c >= Wh) break;
+    auto split = [&](const cpx<S>* z, int c, cpx<S> w) {
         const cpx<S> zk = z[c < L ? c : c - L];
         cpx<S> zc = z[c == 0 ? 0 : L - c];
         zc.y = -zc.y;
         const cpx<S> e = {(zk.x + zc.x) * half, (zk.y + zc.y) * half};
         const cpx<S> o = {(zk.y - zc.y) * half, -(zk.x - zc.x) * half};
-        dst[j * step] = cadd(e, cmul(tw_post[c], o));
+        return cadd(e, cmul(w, o));
+    };
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+        const int c = cb + CS * j;
+        if (j == NJ - 1 && c >= Wh) break;
+        const cpx<S> w = tw_post[c];
+        const cpx<S> x0 = split(z0, c, w), x1 = split(z1, c, w);
+        if constexpr (sizeof(S) == 4) {
+            *reinterpret_cast<float4*>(dst + j * step) = make_float4(x0.x, x0.y, x1.x, x1.y);
+        } else {
+            dst[j * step] = x0;
+            dst[j * step + 1] = x1;
+        }
     }
 }
 
