@@ -91,17 +91,18 @@ __device__ __forceinline__ void rows2_body(const Pix* __restrict__ frames, int H
     __syncthreads();
 
     // even/odd split: X[c] = (Z[c] + conj Z[L-c]) / 2 + W_W^c (Z[c] - conj Z[L-c]) / (2i)
-    // thread (rp, cb) owns rows 2 rp, 2 rp + 1 and the columns c = cb + CS j: fixed strides,
-    // no division, one twiddle load per column for both rows, and the two rows' values of a
-    // column (adjacent in mid[f][col][row]) leave as one 16-byte store (f32)
-    constexpr int RP = RB / 2;                       // row pairs
-    constexpr int CS = kThreads / RP;                // column stride
+    // thread (rq, cb) owns rows RV rq .. RV rq + RV - 1 and the columns c = cb + CS j: fixed
+    // strides, no division, one twiddle load per column for its rows, and those rows' values
+    // of a column (adjacent in mid[f][col][row]) leave as one store: 32 bytes (RV = 4,
+    // st.global.v8) in f32, 16 bytes per two rows in f64
+    constexpr int RV = sizeof(S) == 4 ? 4 : 2;       // rows per thread
+    constexpr int RQ = RB / RV;
+    constexpr int CS = kThreads / RQ;                // column stride
     constexpr int NJ = (Wh + CS - 1) / CS;
     const S half = S(0.5);
-    const int rp = threadIdx.x % RP, cb = threadIdx.x / RP;
-    const cpx<S>* z0 = region_base + (2 * rp) * REG;
-    const cpx<S>* z1 = z0 + REG;
-    cpx<S>* dst = mid + (size_t)fi * Wh * H + r0 + 2 * rp + (size_t)cb * H;
+    const int rq = threadIdx.x % RQ, cb = threadIdx.x / RQ;
+    const cpx<S>* z0 = region_base + (RV * rq) * REG;
+    cpx<S>* dst = mid + (size_t)fi * Wh * H + r0 + RV * rq + (size_t)cb * H;
     const size_t step = (size_t)CS * H;
     auto split = [&](const cpx<S>* z, int c, cpx<S> w) {
         const cpx<S> zk = z[c < L ? c : c - L];
@@ -116,12 +117,17 @@ __device__ __forceinline__ void rows2_body(const Pix* __restrict__ frames, int H
         const int c = cb + CS * j;
         if (j == NJ - 1 && c >= Wh) break;
         const cpx<S> w = tw_post[c];
-        const cpx<S> x0 = split(z0, c, w), x1 = split(z1, c, w);
+        cpx<S> x[RV];
+#pragma unroll
+        for (int r = 0; r < RV; ++r) x[r] = split(z0 + r * REG, c, w);
         if constexpr (sizeof(S) == 4) {
-            *reinterpret_cast<float4*>(dst + j * step) = make_float4(x0.x, x0.y, x1.x, x1.y);
+            asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst + j * step),
+                         "f"(x[0].x), "f"(x[0].y), "f"(x[1].x), "f"(x[1].y), "f"(x[2].x), "f"(x[2].y),
+                         "f"(x[3].x), "f"(x[3].y)
+                         : "memory");
         } else {
-            dst[j * step] = x0;
-            dst[j * step + 1] = x1;
+            dst[j * step] = x[0];
+            dst[j * step + 1] = x[1];
         }
     }
 }
