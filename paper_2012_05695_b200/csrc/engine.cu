@@ -298,7 +298,7 @@ void* Engine::buffer(const std::string& name, size_t bytes) {
 
 bool f32_register_temporal(int N) {
     const int N2 = (int)pad_len(N);
-    return use_warp_temporal(N, N2, 8) || use_long_temporal(N, N2, 8);
+    return use_warp_temporal(N, N2, 4) || use_long_temporal(N, N2, 4);
 }
 
 int64_t max_frames(bool f64) {

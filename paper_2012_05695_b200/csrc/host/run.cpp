@@ -370,8 +370,7 @@ ResultArchive run_core(const Ingest& in, const RunConfig& config, double* out,
         // host while it streams back (exact; half the PCIe bytes). Opt-in: on the measured
         // box 16 host threads widen at ~67 GB/s, about the PCIe rate, so the C2 e2e moved
         // 32.2 -> 31.5 ms in one A/B round and regressed in the other.
-        static const char* widen_env = std::getenv("DDM_D2H_WIDEN");
-        const bool widen = !f64 && total >= (std::int64_t(1) << 22) && widen_env && widen_env[0] == '1' &&
+        const bool widen = !f64 && total >= (std::int64_t(1) << 22) && detail::d2h_widen_enabled() &&
                            b200::f32_register_temporal(N);
         const std::size_t eb = widen ? sizeof(float) : sizeof(double);
         void* d_map = eng.buffer(widen ? "map32" : "map", std::size_t(total) * eb);
@@ -456,6 +455,28 @@ void stream_copy(void* dst, const void* src, std::size_t n) {
         _mm_stream_si128(reinterpret_cast<__m128i*>(d + 48), e);
     }
     std::memcpy(d, s, n - blocks * 64);
+    _mm_sfence();
+}
+
+bool d2h_widen_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("DDM_D2H_WIDEN");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
+// f32 -> f64 (exact) with non-temporal 16-byte stores: the map is written once and read by
+// the caller later, so the stores skip the read-for-ownership of cached stores
+void widen_stream(double* dst, const float* src, std::size_t n) {
+    std::size_t k = 0;
+    for (; k < n && (reinterpret_cast<std::uintptr_t>(dst + k) & 15) != 0; ++k) dst[k] = double(src[k]);
+    for (; k + 4 <= n; k += 4) {
+        const __m128 v = _mm_loadu_ps(src + k);
+        _mm_stream_pd(dst + k, _mm_cvtps_pd(v));
+        _mm_stream_pd(dst + k + 2, _mm_cvtps_pd(_mm_movehl_ps(v, v)));
+    }
+    for (; k < n; ++k) dst[k] = double(src[k]);
     _mm_sfence();
 }
 
@@ -582,9 +603,7 @@ void download_widen(b200::Engine& eng, double* out, const float* d, std::size_t 
             sync.arrive_and_wait();  // chunk i is in slot i & 1
             const std::size_t off = i * kChunk, m = std::min(kChunk, n - off);
             const std::size_t b = m * t / T, e = m * (t + 1) / T;
-            const float* src = pin[i & 1];
-            double* dst = out + off;
-            for (std::size_t k = b; k < e; ++k) dst[k] = double(src[k]);
+            widen_stream(out + off + b, pin[i & 1] + b, e - b);
             sync.arrive_and_wait();  // slot i & 1 is free again
             if (t == 0 && i + 2 < chunks) issue(i + 2);
         }

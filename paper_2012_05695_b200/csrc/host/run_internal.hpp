@@ -70,6 +70,10 @@ bool is_pinned(const void* p);
 // two pinned slots while host threads widen the previous chunk into `out`, so PCIe carries
 // 4 bytes per value instead of 8. Caller holds the engine lock.
 void download_widen(b200::Engine& eng, double* out, const float* d, std::size_t n, cudaStream_t stream);
+// f32 -> f64 with non-temporal stores (run.cpp)
+void widen_stream(double* dst, const float* src, std::size_t n);
+// DDM_D2H_WIDEN=1: f32 maps leave the device as f32 and are widened on the host
+bool d2h_widen_enabled();
 
 // DDM_TRACE=1: wall time of each host phase on stderr ("[tag] phase ms")
 struct Trace {

@@ -100,12 +100,17 @@ TimingBreakdown Session::run_with_ft(const std::int64_t* wv_flat, std::int64_t q
     if (capacity < total) throw InputError("output capacity is smaller than lags x plane");
     spec.groups = {{0, q}};
     cudaStream_t st = eng_->stream();
-    double* d_map = static_cast<double*>(eng_->buffer("map", std::size_t(total) * sizeof(double)));
-    if (!spec.identity) b200::check(cudaMemsetAsync(d_map, 0, std::size_t(total) * sizeof(double), st), "memset");
+    // DDM_D2H_WIDEN=1 (f32 sessions, register temporal engines): the map leaves the device as
+    // f32 (half the PCIe bytes) and is widened on the host (exact)
+    const bool widen = !f64_ && d2h_widen_enabled() && total >= (std::int64_t(1) << 22) &&
+                       b200::f32_register_temporal(N_);
+    const std::size_t eb = widen ? sizeof(float) : sizeof(double);
+    void* d_map = eng_->buffer(widen ? "map32" : "map", std::size_t(total) * eb);
+    if (!spec.identity) b200::check(cudaMemsetAsync(d_map, 0, std::size_t(total) * eb, st), "memset");
     spec.d_out = d_map;
-    spec.out_f64 = true;
+    spec.out_f64 = !widen;
     spec.out_stride = plane;
-    if (is_pinned(out)) spec.host_out = out;
+    if (!widen && is_pinned(out)) spec.host_out = out;
     TimingBreakdown timing;
     b200::PhaseTimes times;
     struct DrainCopies {
@@ -120,7 +125,10 @@ TimingBreakdown Session::run_with_ft(const std::int64_t* wv_flat, std::int64_t q
     eng_->run(spec, &times);
     bool finite = true;
     double peak = 0.0, lowest = 0.0;
-    b200::reduce_stats(d_map, total, st, &finite, &peak, &lowest);
+    if (widen)
+        b200::reduce_stats(static_cast<const float*>(d_map), total, st, &finite, &peak, &lowest);
+    else
+        b200::reduce_stats(static_cast<const double*>(d_map), total, st, &finite, &peak, &lowest);
     const bool streamed = eng_->finish_host_out(&times);
     if (!finite) throw InputError("result map contains non-finite values");
     const double eps = f64_ ? 1e-9 : 1e-4;
@@ -130,7 +138,10 @@ TimingBreakdown Session::run_with_ft(const std::int64_t* wv_flat, std::int64_t q
         timing.merge = times.d2h_ms * 1e-3;
     } else {
         const auto t0 = std::chrono::steady_clock::now();
-        download_pageable(*eng_, out, d_map, std::size_t(total) * sizeof(double), st);
+        if (widen)
+            download_widen(*eng_, out, static_cast<const float*>(d_map), std::size_t(total), st);
+        else
+            download_pageable(*eng_, out, d_map, std::size_t(total) * sizeof(double), st);
         timing.merge = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     }
     timing.step1 = times.spatial_ms * 1e-3;

@@ -28,7 +28,7 @@ def one_stack(sess, frames, out):
                                         C.byref(counters), C.byref(timing)))
 
 
-def main(steps=12, inflight_list=(1, 2, 3)):
+def main(steps=12, inflight_list=(1, 2)):
     rng = np.random.default_rng(5)
     st = rng.integers(0, 4096, size=(N, H, W), dtype=np.uint16)
     results = {}
