@@ -360,13 +360,14 @@ cols2_pair_kernel(const cpx<S>* __restrict__ mid, int Wh, int N, int frame0, int
         cpx<S>* ex = sm + g * B * P;
 #pragma unroll
         for (int k = 0; k < B; ++k) ex[k * P + a] = v[k];
+        asm volatile("bar.sync %0, 64;" ::"r"(1 + g) : "memory");   // this column group only
         {
-            // the row-pass buffer has been consumed: drop its L2 lines without write-back
+            // both warps of the group have their column values (the barrier): drop the
+            // row-pass buffer's L2 lines without write-back
             const char* base = reinterpret_cast<const char*>(col);
             for (int l = a; l < HL * (int)sizeof(cpx<S>) / 128; l += 64)
                 asm volatile("discard.global.L2 [%0], 128;" ::"l"(base + 128 * l) : "memory");
         }
-        asm volatile("bar.sync %0, 64;" ::"r"(1 + g) : "memory");   // this column group only
 #pragma unroll
         for (int a2 = 0; a2 < B; ++a2) v[a2] = ex[k1 * P + 2 * a2 + a1];
         RegDft<B, -1, S>::run(v);
