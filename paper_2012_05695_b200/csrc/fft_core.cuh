@@ -20,24 +20,101 @@ struct alignas(2 * sizeof(S)) cpx {
     S x, y;
 };
 
+// ---------------------------------------------------------------- packed f32x2 (sm_100a)
+// Blackwell issues two f32 lanes per instruction with FADD2 / FMUL2 / FFMA2 (PTX add/sub/
+// mul/fma.rn.f32x2 on a 64-bit register pair). A complex<float> is exactly such a pair, and
+// ptxas folds the FFT's operand shuffles into the instruction's source modifiers: a broadcast
+// of one half (`R.F32`), the swap (`.LO_HI`), the one-half negation (`.NP`, the quarter-turn
+// (-y, x)) and a broadcast immediate. So an add or subtract is one instruction instead of two,
+// a product by a constant or runtime twiddle two instead of four, a + w b two instead of
+// four. Every FFT kernel (spatial, temporal, long) is issue-bound on these, and the roundings
+// are the same fused single-precision operations as the scalar forms. DDM_F32X2=0 restores
+// the scalar code.
+#ifndef DDM_F32X2
+#define DDM_F32X2 1
+#endif
+namespace px {
+using u64 = unsigned long long;
+__device__ __forceinline__ u64 pk(float x, float y) {
+    u64 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(x), "f"(y));
+    return r;
+}
+__device__ __forceinline__ cpx<float> up(u64 r) {
+    cpx<float> a;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a.x), "=f"(a.y) : "l"(r));
+    return a;
+}
+__device__ __forceinline__ u64 add2(u64 a, u64 b) {
+    u64 r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ u64 sub2(u64 a, u64 b) {
+    u64 r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ u64 mul2(u64 a, u64 b) {
+    u64 r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) {
+    u64 r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+}  // namespace px
+
+template <typename S>
+constexpr bool kPacked = DDM_F32X2 && sizeof(S) == 4;
+
 template <typename S>
 __device__ __forceinline__ cpx<S> cmul(cpx<S> a, cpx<S> b) {
-    return {a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x};
+    if constexpr (kPacked<S>) {   // b.x (a.x, a.y) + b.y (-a.y, a.x)
+        using namespace px;
+        return up(fma2(pk(-a.y, a.x), pk(b.y, b.y), mul2(pk(b.x, b.x), pk(a.x, a.y))));
+    } else {
+        return {a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x};
+    }
 }
 // a + w b as two fused multiply-add chains (4 FMA instead of cmul's 4 plus 2 adds)
 template <typename S>
 __device__ __forceinline__ cpx<S> cfma(cpx<S> w, cpx<S> b, cpx<S> a) {
-    return {fma(w.x, b.x, fma(-w.y, b.y, a.x)), fma(w.x, b.y, fma(w.y, b.x, a.y))};
+    if constexpr (kPacked<S>) {   // a + w.x (b.x, b.y) + w.y (-b.y, b.x)
+        using namespace px;
+        return up(fma2(pk(-b.y, b.x), pk(w.y, w.y), fma2(pk(w.x, w.x), pk(b.x, b.y), pk(a.x, a.y))));
+    } else {
+        return {fma(w.x, b.x, fma(-w.y, b.y, a.x)), fma(w.x, b.y, fma(w.y, b.x, a.y))};
+    }
 }
 // 2 a - t: the other butterfly output once t = a + u is known (a - u, 2 FMA)
 template <typename S>
 __device__ __forceinline__ cpx<S> creflect(cpx<S> a, cpx<S> t) {
-    return {fma(S(2), a.x, -t.x), fma(S(2), a.y, -t.y)};
+    if constexpr (kPacked<S>) {
+        using namespace px;
+        return up(fma2(pk(a.x, a.y), pk(2.f, 2.f), pk(-t.x, -t.y)));
+    } else {
+        return {fma(S(2), a.x, -t.x), fma(S(2), a.y, -t.y)};
+    }
 }
 template <typename S>
-__device__ __forceinline__ cpx<S> cadd(cpx<S> a, cpx<S> b) { return {a.x + b.x, a.y + b.y}; }
+__device__ __forceinline__ cpx<S> cadd(cpx<S> a, cpx<S> b) {
+    if constexpr (kPacked<S>) return px::up(px::add2(px::pk(a.x, a.y), px::pk(b.x, b.y)));
+    else return {a.x + b.x, a.y + b.y};
+}
 template <typename S>
-__device__ __forceinline__ cpx<S> csub(cpx<S> a, cpx<S> b) { return {a.x - b.x, a.y - b.y}; }
+__device__ __forceinline__ cpx<S> csub(cpx<S> a, cpx<S> b) {
+    if constexpr (kPacked<S>) return px::up(px::sub2(px::pk(a.x, a.y), px::pk(b.x, b.y)));
+    else return {a.x - b.x, a.y - b.y};
+}
+// s a + b (real s)
+template <typename S>
+__device__ __forceinline__ cpx<S> caxpy(S s, cpx<S> a, cpx<S> b) {
+    if constexpr (kPacked<S>) return px::up(px::fma2(px::pk(s, s), px::pk(a.x, a.y), px::pk(b.x, b.y)));
+    else return {fma(s, a.x, b.x), fma(s, a.y, b.y)};
+}
 // multiply by SIGN * i  (the quarter-turn of the transform direction)
 template <int SIGN, typename S>
 __device__ __forceinline__ cpx<S> rot90(cpx<S> a) {
@@ -165,18 +242,19 @@ __device__ __forceinline__ void dft8_finish(cpx<S>* v) {
         // scalings are fused into the output butterflies: E +- r (O.x -+ ...) as FMAs
         const cpx<S> e1 = v[2], o1 = v[3], e3 = v[6], o3 = v[7];
         // W8^1 O / r  and  W8^3 O / r
-        const cpx<S> u1 = SIGN < 0 ? cpx<S>{o1.x + o1.y, o1.y - o1.x} : cpx<S>{o1.x - o1.y, o1.y + o1.x};
-        const cpx<S> u3 = SIGN < 0 ? cpx<S>{o3.y - o3.x, -(o3.x + o3.y)} : cpx<S>{-(o3.x + o3.y), o3.x - o3.y};
+        // u1 = o1 + rot(o1), u3 = rot(o3) - o3 (rot = the SIGN quarter-turn)
+        const cpx<S> u1 = cadd(o1, rot90<SIGN>(o1));
+        const cpx<S> u3 = csub(rot90<SIGN>(o3), o3);
         v[5] = rot90<SIGN>(v[5]);
         cpx<S> o[8];
         o[0] = cadd(v[0], v[1]);
         o[4] = csub(v[0], v[1]);
-        o[1] = {fma(r, u1.x, e1.x), fma(r, u1.y, e1.y)};
-        o[5] = {fma(-r, u1.x, e1.x), fma(-r, u1.y, e1.y)};
+        o[1] = caxpy(r, u1, e1);
+        o[5] = caxpy(-r, u1, e1);
         o[2] = cadd(v[4], v[5]);
         o[6] = csub(v[4], v[5]);
-        o[3] = {fma(r, u3.x, e3.x), fma(r, u3.y, e3.y)};
-        o[7] = {fma(-r, u3.x, e3.x), fma(-r, u3.y, e3.y)};
+        o[3] = caxpy(r, u3, e3);
+        o[7] = caxpy(-r, u3, e3);
 #pragma unroll
         for (int i = 0; i < 8; ++i) v[i] = o[i];
     }

@@ -38,6 +38,20 @@
 // unfold twiddles W_N2^{-(lane + 32 d)} are loop invariants the compiler would otherwise
 // keep in 64 registers for the kernel's life; they are formed per sequence from an opaque
 // copy of the lane base.
+// K3 keeps the scalar f32 codelets. With the packed FADD2/FFMA2 ones (fft_core.cuh) it
+// issues 20% fewer instructions (5,632 vs 7,000 static) but ran 1.8% slower (0.902 vs
+// 0.886 ms at C2, three interleaved A/B rounds, tools/gpu_ab3.sh): a packed instruction holds
+// the FP32 pipe for two cycles (tools/probes/f32x2_rate.cu: FFMA2 issues at half the scalar
+// rate, equal lane throughput), and at 3 warps per scheduler K3's dependent butterfly chains
+// lose more than the freed issue slots gain. The row/column passes and K3L (more warps, more
+// independent work per lane) gain from them. DDM_F32X2_TW=1 selects them here for A/B builds.
+#ifndef DDM_F32X2
+#ifdef DDM_F32X2_TW
+#define DDM_F32X2 DDM_F32X2_TW
+#else
+#define DDM_F32X2 0
+#endif
+#endif
 #include <algorithm>
 #include <cstdlib>
 
@@ -163,21 +177,15 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
         }
         float mx, my_;
         {
-            float ax[16], ay[16];
+            cpx<float> acc[16];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                ax[i] = v[i].x + v[i + 16].x;
-                ay[i] = v[i].y + v[i + 16].y;
-            }
+            for (int i = 0; i < 16; ++i) acc[i] = cadd(v[i], v[i + 16]);
 #pragma unroll
             for (int w = 8; w > 0; w >>= 1)
 #pragma unroll
-                for (int i = 0; i < w; ++i) {
-                    ax[i] += ax[i + w];
-                    ay[i] += ay[i + w];
-                }
-            mx = ax[0];
-            my_ = ay[0];
+                for (int i = 0; i < w; ++i) acc[i] = cadd(acc[i], acc[i + w]);
+            mx = acc[0].x;
+            my_ = acc[0].y;
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
                 mx += __shfl_xor_sync(0xffffffffu, mx, o);
@@ -190,8 +198,7 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
 #pragma unroll
         for (int b = 0; b < 32; ++b) {
             if (lane + 32 * b < N) {
-                v[b].x -= mx;
-                v[b].y -= my_;
+                v[b] = csub(v[b], cpx<float>{mx, my_});
                 my.stage[lane + 32 * b] = v[b];
             }
         }
