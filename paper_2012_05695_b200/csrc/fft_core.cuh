@@ -67,8 +67,17 @@ __device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) {
 }
 }  // namespace px
 
+#ifndef DDM_F32X2_ADD
+#define DDM_F32X2_ADD DDM_F32X2
+#endif
+#ifndef DDM_F32X2_MUL
+#define DDM_F32X2_MUL DDM_F32X2
+#endif
+// kPacked: products (cmul, cfma, caxpy); kPackedAdd: sums (cadd, csub, creflect)
 template <typename S>
-constexpr bool kPacked = DDM_F32X2 && sizeof(S) == 4;
+constexpr bool kPacked = DDM_F32X2_MUL && sizeof(S) == 4;
+template <typename S>
+constexpr bool kPackedAdd = DDM_F32X2_ADD && sizeof(S) == 4;
 
 template <typename S>
 __device__ __forceinline__ cpx<S> cmul(cpx<S> a, cpx<S> b) {
@@ -92,7 +101,7 @@ __device__ __forceinline__ cpx<S> cfma(cpx<S> w, cpx<S> b, cpx<S> a) {
 // 2 a - t: the other butterfly output once t = a + u is known (a - u, 2 FMA)
 template <typename S>
 __device__ __forceinline__ cpx<S> creflect(cpx<S> a, cpx<S> t) {
-    if constexpr (kPacked<S>) {
+    if constexpr (kPackedAdd<S>) {
         using namespace px;
         return up(fma2(pk(a.x, a.y), pk(2.f, 2.f), pk(-t.x, -t.y)));
     } else {
@@ -101,12 +110,12 @@ __device__ __forceinline__ cpx<S> creflect(cpx<S> a, cpx<S> t) {
 }
 template <typename S>
 __device__ __forceinline__ cpx<S> cadd(cpx<S> a, cpx<S> b) {
-    if constexpr (kPacked<S>) return px::up(px::add2(px::pk(a.x, a.y), px::pk(b.x, b.y)));
+    if constexpr (kPackedAdd<S>) return px::up(px::add2(px::pk(a.x, a.y), px::pk(b.x, b.y)));
     else return {a.x + b.x, a.y + b.y};
 }
 template <typename S>
 __device__ __forceinline__ cpx<S> csub(cpx<S> a, cpx<S> b) {
-    if constexpr (kPacked<S>) return px::up(px::sub2(px::pk(a.x, a.y), px::pk(b.x, b.y)));
+    if constexpr (kPackedAdd<S>) return px::up(px::sub2(px::pk(a.x, a.y), px::pk(b.x, b.y)));
     else return {a.x - b.x, a.y - b.y};
 }
 // s a + b (real s)

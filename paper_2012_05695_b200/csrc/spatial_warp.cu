@@ -12,6 +12,13 @@
 //            one frame; the CTA transposes through shared memory so that each retained wave
 //            vector receives F consecutive frames as one contiguous run:
 //            spec[slot * N + frame] (layout T = 1, consumed by temporal_warp.cu).
+// Packed f32x2 products (FMUL2/FFMA2, fft_core.cuh) but scalar sums in the row and column
+// passes: measured at C2 / C3 / C4 (tools/gpu_ab3.sh, profiles/r02z_f32x2_ab.txt) spatial
+// 0.737 / 6.96 / 66.6 ms scalar, 0.718 / 6.83 / 66.5 all packed, 0.707 / 6.76 / 65.6 with
+// products only (FADD2 alone: 0.777 at C2). K3L (temporal_long2.cu) keeps both packed.
+#ifndef DDM_F32X2_ADD
+#define DDM_F32X2_ADD 0
+#endif
 #include <algorithm>
 #include <cstdlib>
 #include <type_traits>
