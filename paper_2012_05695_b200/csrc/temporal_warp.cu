@@ -26,8 +26,8 @@
 // 117 KB unrolled kernel raised instruction-fetch stalls from 0.17 to 0.46 per issue.
 //
 // Data movement per sequence: one TMA bulk copy (cp.async.bulk, 8 KB) into the warp's stage.
-// The first pass writes the shifted sequence back; the odd transform re-reads it and leaves
-// |t|^2 in its place for the averages term; once that has been read the next sequence's copy
+// The first pass shifts the sequence in registers; the odd transform re-reads and re-shifts
+// it and leaves |t|^2 in its place for the averages term; once that has been read the next sequence's copy
 // is issued, so it lands during the S(m) scan, the unfold and the tile store (an L2 prefetch
 // of the same bytes goes out one sequence earlier). Three four-step FFTs (warp_fft.cuh, one
 // shared-memory exchange each); the exchange buffer then holds S(m) and d(m); the
@@ -194,14 +194,12 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
             mx *= inv_nf;
             my_ *= inv_nf;
         }
-        // shift once and write t back: the odd transform re-reads the shifted sequence
+        // shift in registers; the odd transform re-reads the raw sequence and shifts it again
+        // (writing the shifted sequence back cost 64 shared-memory wavefronts per sequence,
+        // K3's busiest unit: 0.887 vs 0.880 ms measured, profiles/r02z_f32x2_ab.txt)
 #pragma unroll
-        for (int b = 0; b < 32; ++b) {
-            if (lane + 32 * b < N) {
-                v[b] = csub(v[b], cpx<float>{mx, my_});
-                my.stage[lane + 32 * b] = v[b];
-            }
-        }
+        for (int b = 0; b < 32; ++b)
+            if (lane + 32 * b < N) v[b] = csub(v[b], cpx<float>{mx, my_});
 
         // map mode: the previous tile's d values sit in every warp's exchange buffer until
         // the CTA has stored them; the store overlaps this sequence's copy wait and mean
@@ -214,12 +212,12 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
 #pragma unroll
         for (int d = 0; d < 32; ++d) pe[d] = v[d].x * v[d].x + v[d].y * v[d].y;
 
-        // ---- odd outputs: t again from the stage; its last read, so |t|^2 (f32, of the
+        // ---- odd outputs: t again from the stage (shifted again); its last read, so |t|^2 (f32, of the
         //      shifted sequence) replaces it there for the averages term
 #pragma unroll
         for (int b = 0; b < 32; ++b) {
             const int n = lane + 32 * b;
-            v[b] = (n < N) ? my.stage[n] : cpx<float>{0.f, 0.f};
+            v[b] = (n < N) ? csub(my.stage[n], cpx<float>{mx, my_}) : cpx<float>{0.f, 0.f};
         }
         __syncwarp();
         float* pw = reinterpret_cast<float*>(my.stage);   // |t|^2 at padded(n)
