@@ -423,7 +423,10 @@ namespace {
 // Warps (wave vectors) per CTA, one CTA per SM: 12 in map mode (168 registers without
 // spills, the unfold twiddles are not hoisted; 218 KB of shared memory), 8 in ring mode (its
 // per-warp ring accumulators need 4 KB more per warp).
-constexpr int kTW = 12;
+#ifndef DDM_K3_WARPS
+#define DDM_K3_WARPS 12
+#endif
+constexpr int kTW = DDM_K3_WARPS;
 constexpr int kTWRing = 8;
 
 template <typename OutT, bool kDiag, bool kRing>
