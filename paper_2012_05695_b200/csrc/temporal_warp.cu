@@ -38,21 +38,27 @@
 // unfold twiddles W_N2^{-(lane + 32 d)} are loop invariants the compiler would otherwise
 // keep in 64 registers for the kernel's life; they are formed per sequence from an opaque
 // copy of the lane base.
-// K3 keeps the scalar f32 codelets. With the packed FADD2/FFMA2 ones (fft_core.cuh) it
-// issues 20% fewer instructions (5,632 vs 7,000 static) but ran 1.8% slower (0.902 vs
-// 0.886 ms at C2, three interleaved A/B rounds, tools/gpu_ab3.sh): a packed instruction holds
-// the FP32 pipe for two cycles (tools/probes/f32x2_rate.cu: FFMA2 issues at half the scalar
-// rate, equal lane throughput), and at 3 warps per scheduler K3's dependent butterfly chains
-// lose more than the freed issue slots gain. The row/column passes and K3L (more warps, more
-// independent work per lane) gain from them, and so does K3's own ring mode at 8 warps per
-// SM (temporal_warp_ring.cu). DDM_F32X2_TW=1 selects them here for A/B builds.
+// K3 runs the packed f32x2 codelets (fft_core.cuh: FADD2/FMUL2/FFMA2, 20% fewer issued
+// instructions). They first measured 1.8% slower (0.902 vs 0.886 ms at C2): the register
+// pairs pushed K3 past its 168-register cap (12 warps per SM) and the spill reloads sat on the
+// tile loop. With the tile store's addressing recomputed per tile (the thread index re-read
+// in temporal_warp_kernel.cuh, so the 64-bit row offsets are not held through the
+// transforms) only the copy phase bit spills and K3 runs 0.867 ms against 0.878 ms scalar
+// (three interleaved A/B rounds, tools/gpu_ab3.sh, profiles/r02z_f32x2_ab.txt). The scalar
+// codelets with that change measured 0.885 ms (the hoisted addressing suits them).
+// Sums stay scalar (FADD; products packed), as in the row/column passes: 0.865 vs 0.867 ms.
+// DDM_F32X2_TW=0 selects the scalar codelets for A/B builds. The ring mode (8 warps per SM)
+// is in temporal_warp_ring.cu.
 // The kernel template and its launcher live in temporal_warp_kernel.cuh.
 #ifndef DDM_F32X2
 #ifdef DDM_F32X2_TW
 #define DDM_F32X2 DDM_F32X2_TW
 #else
-#define DDM_F32X2 0
+#define DDM_F32X2 1
 #endif
+#endif
+#ifndef DDM_F32X2_ADD
+#define DDM_F32X2_ADD 0
 #endif
 #include "temporal_warp_kernel.cuh"
 

@@ -312,8 +312,13 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
             return reinterpret_cast<const float*>(ws[j].scratch)[padded(m)];
         };
         const int64_t q0 = tile * kWarps;
+        // the thread index re-read per tile: keeps the compiler from hoisting the store
+        // addressing (64-bit row offsets and strides) out of the tile loop, where it would
+        // hold registers through the transforms
+        unsigned tid;
+        asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tid));
         if (!lag_index && !dest_of_slot && q0 + kWarps <= nq) {
-            OutT* dst = out + (int64_t)threadIdx.x * out_stride + q0;
+            OutT* dst = out + (int64_t)tid * out_stride + q0;
             const int64_t step = (int64_t)blockDim.x * out_stride;
             if (vec_store) {
                 // TPR threads cover one lag row's run of kWarps values (48 B f32 / 96 B f64 at
@@ -322,12 +327,12 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
                 constexpr int VPT = 16 / (int)sizeof(OutT);
                 constexpr int TPR = kWarps / VPT;
                 static_assert(kWarps % VPT == 0, "whole 16-byte vectors per row");
-                const int k = threadIdx.x % TPR;
+                const int k = tid % TPR;
                 const int rows = blockDim.x / TPR;
-                OutT* pdst = out + (int64_t)(threadIdx.x / TPR) * out_stride + q0 + VPT * k;
+                OutT* pdst = out + (int64_t)(tid / TPR) * out_stride + q0 + VPT * k;
                 const int64_t pstep = (int64_t)rows * out_stride;
 #pragma unroll 4
-                for (int m = threadIdx.x / TPR; m < N; m += rows, pdst += pstep) {
+                for (int m = tid / TPR; m < N; m += rows, pdst += pstep) {
                     if constexpr (VPT == 4) {
                         float4 v4;
                         v4.x = dval(4 * k + 0, m);
@@ -343,14 +348,14 @@ temporal_warp_kernel(const cpx<float>* __restrict__ spec, const __grid_constant_
                     }
                 }
             } else {
-                for (int m = threadIdx.x; m < N; m += blockDim.x, dst += step) {
+                for (int m = tid; m < N; m += blockDim.x, dst += step) {
 #pragma unroll
                     for (int j = 0; j < kWarps; ++j)
                         dst[j] = (OutT)dval(j, m);
                 }
             }
         } else {
-            for (int idx = threadIdx.x; idx < N * kWarps; idx += blockDim.x) {
+            for (int idx = tid; idx < N * kWarps; idx += blockDim.x) {
                 const int m = idx / kWarps, j = idx - m * kWarps;
                 if (q0 + j >= nq) continue;
                 const int li = lag_index ? lag_index[m] : m;
