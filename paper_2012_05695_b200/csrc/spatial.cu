@@ -152,7 +152,9 @@ int pick_rows(int L, size_t scalar_bytes, bool naive) {
 template <typename S, typename Pix, int LC>
 void launch_rows(const SpatialArgs& a, int RB, const FftPlan& plan, size_t smem, cudaStream_t st) {
     auto k = rows_kernel<S, Pix, LC>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // a failed attribute stays the last error (the caller's cudaGetLastError reports it):
+    // no launch that would fail later with an unrelated message
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return;
     const int grid = a.nframes * ((a.H + RB - 1) / RB);
     k<<<grid, kThreads, smem, st>>>(static_cast<const Pix*>(a.frames), a.W, a.H, a.frame0, RB,
                                     plan, static_cast<const cpx<S>*>(a.tw_row.ptr),
@@ -163,7 +165,9 @@ void launch_rows(const SpatialArgs& a, int RB, const FftPlan& plan, size_t smem,
 template <typename S, int LC>
 void launch_cols(const SpatialArgs& a, int CB, int F, const FftPlan& plan, size_t smem, cudaStream_t st) {
     auto k = cols_kernel<S, LC>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // a failed attribute stays the last error (the caller's cudaGetLastError reports it):
+    // no launch that would fail later with an unrelated message
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return;
     const int Wh = a.W / 2 + 1;
     const int grid = ((a.nframes + F - 1) / F) * ((Wh + CB - 1) / CB);
     k<<<grid, kThreads, smem, st>>>(static_cast<const cpx<S>*>(a.mid), a.H, Wh, CB, F, a.nframes, a.N,

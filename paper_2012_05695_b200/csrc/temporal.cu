@@ -263,7 +263,9 @@ void launch_t(const TemporalArgs& a, cudaStream_t stream) {
     const size_t smem = temporal_smem_bytes(a.N, N2, T, sizeof(S));
     const int threads = temporal_threads(N2, T, sizeof(S));
     auto k = threads == 512 ? temporal_kernel<S, OutT, N2, 512> : temporal_kernel<S, OutT, N2, 256>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // a failed attribute stays the last error (the caller's cudaGetLastError reports it):
+    // no launch that would fail later with an unrelated message
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return;
     k<<<(unsigned)a.layout.tiles(), threads, smem, stream>>>(
         static_cast<const cpx<S>*>(a.spec), a.N, a.layout, static_cast<const cpx<S>*>(a.tw.ptr),
         static_cast<const cpx<S>*>(a.tw_half.ptr),
